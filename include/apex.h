@@ -1,0 +1,172 @@
+/*
+ * apex.h — C ABI of the B200-native APEX decode-attention hot path.
+ *
+ * What the library computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   Decode-phase self-attention over a growing KV cache (§2.1: each
+ *   layer caches one K and one V vector per token; decode generates one token
+ *   per step), memory-bandwidth-bound (§2.2), with GQA K/V sharing,
+ *   the cache managed in fixed-size blocks like the paper's "Paged Attention"
+ *   backends (§4.1) and handled dynamically (§3.1), plus the
+ *   profiling-informed time prediction of §3.1/§3.2.
+ *   Per request b and query head h (kv head g = h / (Hq/Hkv)):
+ *       out[b,h,:] = softmax_t(scale * q[b,h,:] . K[b,g,t,:]) . V[b,g,t,:]
+ *   over t = 0 .. len_b-1 (BASELINE.json north_star states the formula;
+ *   DESIGN.md "Readings" c1-c16 list every interpretation of a silence).
+ *
+ * Conventions
+ *   - Every call returns apex_status; nothing throws or aborts across the ABI.
+ *     On a non-OK status apex_last_error() returns a thread-local message.
+ *   - Device pointers are CUDA device addresses owned by the CALLER (here:
+ *     torch tensors).  Host pointers are plain host memory, read during the
+ *     call only.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream); every device operation is enqueued on it and no call
+ *     synchronises the device.
+ *   - All calls that enqueue work for one handle must be issued on one stream
+ *     (or ordered by the caller): apex_kv_alloc uploads the step's metadata into
+ *     the workspace that apex_kv_append / apex_decode_attention read.
+ *   - A handle is not thread-safe; use one handle per (process, GPU, model).
+ *   - Host-only handles (desc.k_pool == NULL and desc.block_table == NULL) run
+ *     the allocator and planner without any CUDA call; append/decode then
+ *     return APEX_EINVAL.  Used by CPU tests and host-side planning.
+ */
+#ifndef APEX_H
+#define APEX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    APEX_OK = 0,
+    APEX_EINVAL = 1,        /* bad argument / state; nothing was changed or enqueued */
+    APEX_ENOBLOCKS = 2,     /* KV pool exhausted; the alloc call changed nothing */
+    APEX_ESEQ = 3,          /* unknown or already-released sequence id */
+    APEX_ECUDA = 4,         /* a CUDA runtime/driver call or launch failed */
+    APEX_EUNSUPPORTED = 5   /* valid but unsupported shape/dtype combination */
+} apex_status;
+
+typedef enum { APEX_F32 = 0, APEX_F16 = 1, APEX_BF16 = 2 } apex_dtype;  /* KV, q and out share it */
+
+typedef struct apex_kv apex_kv;
+typedef struct apex_cost apex_cost;
+typedef void *apex_stream;   /* cudaStream_t */
+
+typedef struct {
+    int32_t num_layers;          /* physical layers that own a pool pair (1..64) */
+    int32_t num_q_heads;         /* Hq (local to this rank when heads are sharded) */
+    int32_t num_kv_heads;        /* Hkv; Hq % Hkv == 0, group g = Hq/Hkv in {1,2,4,8} */
+    int32_t head_dim;            /* D; must be 128 */
+    int32_t block_size;          /* tokens per KV block; must be 16 (reading c9) */
+    int32_t num_blocks;          /* blocks in each pool */
+    int32_t max_seqs;            /* sequence ids are 0 .. max_seqs-1 (rows of block_table) */
+    int32_t max_blocks_per_seq;  /* columns of block_table; max context = this * block_size */
+    int32_t max_batch;           /* max sequences in one apex_kv_alloc call (decode batch) */
+    int32_t max_new_tokens;      /* max sum(n_new) in one apex_kv_alloc call */
+    apex_dtype dtype;
+    /* [num_layers] device pointers; each pool is [num_blocks][Hkv][block_size][D]
+       elements of `dtype`, 128-byte aligned.  Pools may alias (logical layers
+       mapped onto fewer physical layers is the caller's choice). */
+    void *const *k_pool;
+    void *const *v_pool;
+    int32_t *block_table;        /* device int32 [max_seqs][max_blocks_per_seq] */
+    int32_t *seq_lens;           /* device int32 [max_seqs] */
+    void *workspace;             /* device scratch, >= apex_kv_workspace_bytes(desc), 256-B aligned */
+    size_t workspace_bytes;
+} apex_kv_desc;
+
+/* Device workspace the handle needs for this desc (step metadata, work list,
+   split-KV partials).  Returns 0 if the desc is invalid. */
+size_t apex_kv_workspace_bytes(const apex_kv_desc *desc);
+
+/* Validate the desc, build the LIFO free list (first pop = block 0, reading
+   c10), the host mirrors, the pinned staging ring and one TMA descriptor per
+   (physical layer, K/V).  Launches no kernel.  The pools' contents are not
+   touched (callers may pre-fill them, e.g. with NaN in tests). */
+apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out);
+
+/* Free host state.  The caller must synchronise its streams first. */
+void apex_kv_destroy(apex_kv *kv);
+
+/* Reserve slots for this step and DEFINE THE STEP BATCH.
+   seq_ids[i] (unique, 0..max_seqs-1) gains n_new[i] >= 0 tokens; a sequence
+   with length 0 is new.  Batch row i of q/out is seq_ids[i]; the k_new/v_new
+   rows of apex_kv_append are the n_new[i] rows of each seq, concatenated in
+   call order.  A block is popped only when a token lands at pos % 16 == 0.
+   All-or-nothing: APEX_ENOBLOCKS / APEX_EINVAL leave every state unchanged.
+   Lengths after the call must be in [1, max_blocks_per_seq*16].  Enqueues one
+   H2D copy of the step metadata (block-table/length deltas, slot mapping,
+   split-KV work list) and one small kernel that applies the deltas to
+   block_table / seq_lens on `stream`.  n in [1, max_batch]. */
+apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_new, int32_t n,
+                          apex_stream stream);
+
+/* Return the sequence's blocks to the free list in reverse table order (so
+   they are popped again in table order) and forget it.  Host-only: the device
+   block_table row is left stale (it is never read for a released sequence). */
+apex_status apex_kv_release(apex_kv *kv, int32_t seq_id);
+
+/* Write this step's new K and V vectors of physical layer `layer` into the
+   pools (one K and one V vector per token per layer).  k_new, v_new:
+   device [sum(n_new)][Hkv][D] of dtype, rows ordered as defined by the last
+   apex_kv_alloc.  Bit-exact copy: K_pool[layer][blk][h][t][:] = k_new[row][h][:]
+   with (blk, t) from the row's slot.  One kernel launch. */
+apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const void *v_new,
+                           apex_stream stream);
+
+/* Decode attention of the last alloc's batch against physical layer `layer`.
+   q: device [B][Hq][D] of dtype (post-RoPE queries, one row per seq in alloc
+   order); out: device [B][Hq][D] of dtype (rounded to nearest even once, from
+   fp32).  Attends over seq_lens[seq] tokens, INCLUDING this step's appended
+   token (reading c3).  scale is usually 1/sqrt(D) (reading c1).  Split-KV
+   flash-decode (FlashDecoding lineage): one persistent kernel over the
+   planned work items + (if any (seq, kv-head) was split) one log-sum-exp
+   merge kernel.  Results are deterministic and independent of the physical
+   block placement.  Supported: F32/F16 with g == 1 (CUDA cores), F16/BF16
+   with g in {2,4,8} (tensor cores, mma.sync); otherwise APEX_EUNSUPPORTED. */
+apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out,
+                                  float scale, apex_stream stream);
+
+/* ---- planner knobs and introspection (host state only; no CUDA calls) ---- */
+
+/* Split-KV chunk in tokens (multiple of 16) used by the NEXT apex_kv_alloc;
+   0 = automatic.  A fixed chunk makes results bit-identical across request /
+   head sharding (tests).  APEX_EINVAL if not a multiple of block_size or < 0. */
+apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens);
+/* Number of persistent CTAs the planner targets (0 = device default). */
+apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas);
+int32_t apex_kv_num_free_blocks(const apex_kv *kv);
+/* len and block ids (table order) of a live sequence; *n_blocks may exceed cap
+   (then only cap ids are written). */
+apex_status apex_kv_seq_info(const apex_kv *kv, int32_t seq_id, int32_t *len, int32_t *blocks,
+                             int32_t cap, int32_t *n_blocks);
+/* slot (= block*block_size + offset) of every new-token row of the last alloc */
+apex_status apex_kv_last_slots(const apex_kv *kv, int32_t *slots, int32_t cap, int32_t *n);
+/* last alloc's work list: 6 int32 per item {batch row, kv head, first logical
+   block, n blocks, partial slot or -1, seq id}, in execution-priority order */
+apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t *n_items,
+                         int32_t *n_merges);
+
+/* ---- profiling-informed time prediction ---- */
+
+/* Table of measured per-layer-call decode-attention times us[i*nk + j] at
+   (batch[i], kv_tokens[j]).  Grids strictly increasing and positive; times
+   finite and > 0; nb, nk >= 1.  Copies the table. */
+apex_status apex_cost_create(const int32_t *batch, int32_t nb, const int64_t *kv_tokens, int32_t nk,
+                             const double *us, apex_cost **out);
+/* Bilinear interpolation over (batch, total kv tokens of the batch), clamped to
+   the grid's edges on each axis (reading c16).  Pure host computation. */
+apex_status apex_predict_time(const apex_cost *cost, int32_t batch, int64_t kv_tokens,
+                              double *us_out);
+void apex_cost_destroy(apex_cost *cost);
+
+/* Thread-local text for the last non-OK status of this thread ("" if none). */
+const char *apex_last_error(void);
+const char *apex_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APEX_H */

@@ -1,0 +1,605 @@
+// Host core of the C ABI declared in include/apex.h: paged-KV allocator with a
+// host mirror of the block table, split-KV planner, pinned staging of the step
+// metadata, TMA descriptor setup, kernel dispatch and the cost model.
+//
+// Paper anchors (PAPER.md line numbers): KV cache of one K and one V vector per
+// token per layer, "handled dynamically" KV management, paged
+// attention backends, decode attention, offline
+// profiler + performance model.  Allocation contract:
+// DESIGN.md reading c10.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "apex_internal.h"
+
+using apex::MergeItem;
+using apex::WorkItem;
+
+namespace {
+
+thread_local std::string g_err;
+
+apex_status fail(apex_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+apex_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(APEX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int elem_bytes(apex_dtype dt) { return dt == APEX_F32 ? 4 : 2; }
+
+bool desc_host_only(const apex_kv_desc *d) { return d->k_pool == nullptr && d->block_table == nullptr; }
+
+int query_sm_count(bool host_only) {
+    if (host_only) return 148;
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        return 148;
+    }
+    return n;
+}
+
+// Device workspace layout.  Every step uploads one packed region (items,
+// merges, slots, block-table deltas, length deltas) into `upload`.
+struct WsLayout {
+    int32_t max_items = 0, max_merges = 0, max_bt_delta = 0;
+    size_t counters = 0, upload = 0, upload_cap = 0, part_o = 0, part_ml = 0, total = 0;
+};
+
+WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
+    WsLayout w;
+    const int G = d->num_q_heads / d->num_kv_heads;
+    const int64_t pairs = (int64_t)d->max_batch * d->num_kv_heads;
+    // auto planner: items <= pairs + 16 * grid; grid <= 4 * SMs
+    w.max_items = (int32_t)std::min<int64_t>(pairs + 16LL * 4 * sm_count + 64, 1 << 24);
+    w.max_merges = (int32_t)pairs;
+    w.max_bt_delta = (int32_t)(cdiv(d->max_new_tokens, d->block_size) + d->max_batch);
+    size_t up = 0;
+    up += align_up(sizeof(WorkItem) * (size_t)w.max_items, 256);
+    up += align_up(sizeof(MergeItem) * (size_t)w.max_merges, 256);
+    up += align_up(sizeof(int32_t) * (size_t)d->max_new_tokens, 256);
+    up += align_up(sizeof(int2) * (size_t)w.max_bt_delta, 256);
+    up += align_up(sizeof(int2) * (size_t)d->max_batch, 256);
+    w.counters = 0;
+    w.upload = 512;                                           // 2 counters x 64 layers
+    w.upload_cap = up;
+    w.part_o = align_up(w.upload + up, 256);
+    w.part_ml = align_up(w.part_o + sizeof(float) * (size_t)w.max_items * G * d->head_dim, 256);
+    w.total = align_up(w.part_ml + sizeof(float) * 2 * (size_t)w.max_items * G, 256);
+    return w;
+}
+
+apex_status validate_desc(const apex_kv_desc *d) {
+    if (!d) return fail(APEX_EINVAL, "desc is NULL");
+    if (d->num_layers < 1 || d->num_layers > apex::kMaxLayers)
+        return fail(APEX_EINVAL, "num_layers %d not in [1, %d]", d->num_layers, apex::kMaxLayers);
+    if (d->num_q_heads < 1 || d->num_kv_heads < 1 || d->num_q_heads % d->num_kv_heads)
+        return fail(APEX_EINVAL, "num_q_heads %d must be a positive multiple of num_kv_heads %d",
+                    d->num_q_heads, d->num_kv_heads);
+    if (d->num_kv_heads > 1024 || d->num_q_heads > 4096) return fail(APEX_EINVAL, "too many heads");
+    const int G = d->num_q_heads / d->num_kv_heads;
+    if (d->head_dim != apex::kHeadDim) return fail(APEX_EUNSUPPORTED, "head_dim %d (only 128)", d->head_dim);
+    if (d->block_size != apex::kBlock) return fail(APEX_EUNSUPPORTED, "block_size %d (only 16)", d->block_size);
+    if (d->dtype != APEX_F32 && d->dtype != APEX_F16 && d->dtype != APEX_BF16)
+        return fail(APEX_EINVAL, "unknown dtype %d", (int)d->dtype);
+    if (!apex::decode_supported(d->dtype, G))
+        return fail(APEX_EUNSUPPORTED, "dtype %d with group %d (supported: F32/F16 g=1, F16/BF16 g in {2,4,8})",
+                    (int)d->dtype, G);
+    if (d->num_blocks < 1 || d->max_seqs < 1 || d->max_blocks_per_seq < 1 || d->max_batch < 1 ||
+        d->max_new_tokens < 1)
+        return fail(APEX_EINVAL, "num_blocks/max_seqs/max_blocks_per_seq/max_batch/max_new_tokens must be >= 1");
+    if ((int64_t)d->max_blocks_per_seq * d->block_size > (1LL << 30))
+        return fail(APEX_EINVAL, "max context too large");
+    if ((int64_t)d->num_blocks * d->num_kv_heads * d->block_size >= (1LL << 31))
+        return fail(APEX_EUNSUPPORTED, "pool rows exceed the TMA coordinate range");
+    if (d->max_batch > d->max_seqs) return fail(APEX_EINVAL, "max_batch > max_seqs");
+    if (!desc_host_only(d)) {
+        if (!d->k_pool || !d->v_pool || !d->block_table || !d->seq_lens || !d->workspace)
+            return fail(APEX_EINVAL, "device desc needs k_pool, v_pool, block_table, seq_lens, workspace");
+        for (int l = 0; l < d->num_layers; ++l) {
+            if (!d->k_pool[l] || !d->v_pool[l]) return fail(APEX_EINVAL, "pool pointer of layer %d is NULL", l);
+            if (((uintptr_t)d->k_pool[l] | (uintptr_t)d->v_pool[l]) & 127)
+                return fail(APEX_EINVAL, "pools of layer %d are not 128-byte aligned", l);
+        }
+        if ((uintptr_t)d->workspace & 255) return fail(APEX_EINVAL, "workspace not 256-byte aligned");
+    }
+    return APEX_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// TMA view of one pool: rows = (block*Hkv + head)*16 + t, each row D elements.
+// Preferred 3-D view {128-B segment elements, rows, segments} with 128-B
+// swizzle loads a whole (block, head) tile with ONE cp.async.bulk.tensor into
+// smem laid out [segment][16 rows][128 B]; the 2-D fallback issues one op per
+// segment into the same layout.
+bool encode_pool(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap *m, void *base, apex_dtype dt,
+                 int64_t rows, int segs_mode) {
+    const int es = elem_bytes(dt);
+    const CUtensorMapDataType tdt = dt == APEX_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                    : dt == APEX_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                     : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const cuuint64_t row_bytes = (cuuint64_t)apex::kHeadDim * es;
+    const cuuint32_t seg_elems = 128 / es, segs = (cuuint32_t)(row_bytes / 128);
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r;
+    if (segs_mode == 1) {
+        cuuint64_t dims[3] = {seg_elems, (cuuint64_t)rows, segs};
+        cuuint64_t strides[2] = {row_bytes, 128};
+        cuuint32_t box[3] = {seg_elems, (cuuint32_t)apex::kBlock, segs};
+        r = enc(m, tdt, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[2] = {(cuuint64_t)apex::kHeadDim, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {row_bytes};
+        cuuint32_t box[2] = {seg_elems, (cuuint32_t)apex::kBlock};
+        r = enc(m, tdt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct apex_kv {
+    apex_kv_desc d{};
+    std::vector<void *> k_pools, v_pools;
+    bool host_only = true;
+    int sm_count = 148;
+    int group = 1;
+    WsLayout ws;
+    int32_t forced_chunk_blocks = 0;
+    int32_t grid_override = 0;
+
+    struct Seq {
+        bool live = false;
+        int32_t len = 0;
+        std::vector<int32_t> blocks;
+    };
+    std::vector<int32_t> free_stack;   // back() is popped first
+    std::vector<Seq> seqs;
+
+    // the current step (defined by the last successful apex_kv_alloc)
+    bool have_step = false;
+    int32_t batch = 0, n_rows = 0;
+    std::vector<int32_t> batch_seq, slots;
+    std::vector<WorkItem> items;
+    std::vector<MergeItem> merges;
+    const WorkItem *d_items = nullptr;
+    const MergeItem *d_merges = nullptr;
+    const int32_t *d_slots = nullptr;
+
+    // pinned staging ring for the per-step upload
+    uint8_t *staging[2] = {nullptr, nullptr};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
+    bool staged_pending[2] = {false, false};
+    int ring = 0;
+
+    std::vector<apex::TmaPair> tmaps;
+    int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
+};
+
+extern "C" {
+
+const char *apex_last_error(void) { return g_err.c_str(); }
+const char *apex_version(void) { return "apex-b200 0.1 (sm_100a)"; }
+
+size_t apex_kv_workspace_bytes(const apex_kv_desc *desc) {
+    if (validate_desc(desc) != APEX_OK) return 0;
+    return layout_for(desc, query_sm_count(desc_host_only(desc))).total;
+}
+
+apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
+    if (!out) return fail(APEX_EINVAL, "out is NULL");
+    *out = nullptr;
+    apex_status st = validate_desc(desc);
+    if (st != APEX_OK) return st;
+    apex_kv *kv = new (std::nothrow) apex_kv();
+    if (!kv) return fail(APEX_EINVAL, "out of host memory");
+    kv->d = *desc;
+    kv->host_only = desc_host_only(desc);
+    kv->group = desc->num_q_heads / desc->num_kv_heads;
+    kv->sm_count = query_sm_count(kv->host_only);
+    kv->ws = layout_for(desc, kv->sm_count);
+    kv->seqs.resize(desc->max_seqs);
+    kv->free_stack.resize(desc->num_blocks);
+    for (int32_t i = 0; i < desc->num_blocks; ++i) kv->free_stack[i] = desc->num_blocks - 1 - i;
+    if (!kv->host_only) {
+        if (desc->workspace_bytes < kv->ws.total) {
+            delete kv;
+            return fail(APEX_EINVAL, "workspace_bytes %zu < required %zu", desc->workspace_bytes,
+                        (size_t)apex_kv_workspace_bytes(desc));
+        }
+        kv->k_pools.assign(desc->k_pool, desc->k_pool + desc->num_layers);
+        kv->v_pools.assign(desc->v_pool, desc->v_pool + desc->num_layers);
+        kv->d.k_pool = kv->k_pools.data();
+        kv->d.v_pool = kv->v_pools.data();
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = cudaHostAlloc((void **)&kv->staging[i], kv->ws.upload_cap, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->staged[i], cudaEventDisableTiming);
+            if (e != cudaSuccess) {
+                apex_kv_destroy(kv);
+                return cuda_fail(e, "apex_kv_create: pinned staging");
+            }
+        }
+        auto enc = get_encode();
+        if (!enc) {
+            apex_kv_destroy(kv);
+            return fail(APEX_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        }
+        const int64_t rows = (int64_t)desc->num_blocks * desc->num_kv_heads * desc->block_size;
+        kv->tmaps.resize(desc->num_layers);
+        for (int mode : {1, 2}) {
+            bool ok = true;
+            for (int l = 0; l < desc->num_layers && ok; ++l)
+                ok = encode_pool(enc, &kv->tmaps[l].k, kv->k_pools[l], desc->dtype, rows, mode) &&
+                     encode_pool(enc, &kv->tmaps[l].v, kv->v_pools[l], desc->dtype, rows, mode);
+            if (ok) {
+                kv->tma_segs = mode == 1 ? 1 : apex::kHeadDim * elem_bytes(desc->dtype) / 128;
+                break;
+            }
+            if (mode == 2) {
+                apex_kv_destroy(kv);
+                return fail(APEX_ECUDA, "cuTensorMapEncodeTiled rejected the pool layout");
+            }
+        }
+        cudaError_t e = apex::decode_prepare(desc->dtype, kv->group);
+        if (e != cudaSuccess) {
+            apex_kv_destroy(kv);
+            return cuda_fail(e, "apex_kv_create: decode kernel attributes");
+        }
+        // zero the work-queue counters once; kernels leave them at zero
+        e = cudaMemset((uint8_t *)desc->workspace + kv->ws.counters, 0, 512);
+        if (e != cudaSuccess) {
+            apex_kv_destroy(kv);
+            return cuda_fail(e, "apex_kv_create: counters");
+        }
+    }
+    *out = kv;
+    return APEX_OK;
+}
+
+void apex_kv_destroy(apex_kv *kv) {
+    if (!kv) return;
+    for (int i = 0; i < 2; ++i) {
+        if (kv->staged[i]) cudaEventDestroy(kv->staged[i]);
+        if (kv->staging[i]) cudaFreeHost(kv->staging[i]);
+    }
+    delete kv;
+}
+
+apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (chunk_tokens < 0 || chunk_tokens % kv->d.block_size)
+        return fail(APEX_EINVAL, "chunk_tokens %d must be a non-negative multiple of %d", chunk_tokens,
+                    kv->d.block_size);
+    kv->forced_chunk_blocks = chunk_tokens / kv->d.block_size;
+    return APEX_OK;
+}
+
+apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas) {
+    if (!kv || ctas < 0) return fail(APEX_EINVAL, "bad grid override");
+    kv->grid_override = ctas;
+    return APEX_OK;
+}
+
+int32_t apex_kv_num_free_blocks(const apex_kv *kv) { return kv ? (int32_t)kv->free_stack.size() : -1; }
+
+apex_status apex_kv_seq_info(const apex_kv *kv, int32_t seq_id, int32_t *len, int32_t *blocks, int32_t cap,
+                             int32_t *n_blocks) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (seq_id < 0 || seq_id >= kv->d.max_seqs || !kv->seqs[seq_id].live)
+        return fail(APEX_ESEQ, "sequence %d is not live", seq_id);
+    const auto &s = kv->seqs[seq_id];
+    if (len) *len = s.len;
+    if (n_blocks) *n_blocks = (int32_t)s.blocks.size();
+    if (blocks)
+        for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)s.blocks.size()); ++i) blocks[i] = s.blocks[i];
+    return APEX_OK;
+}
+
+apex_status apex_kv_last_slots(const apex_kv *kv, int32_t *slots, int32_t cap, int32_t *n) {
+    if (!kv || !kv->have_step) return fail(APEX_EINVAL, "no step allocated");
+    if (n) *n = (int32_t)kv->slots.size();
+    if (slots)
+        for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)kv->slots.size()); ++i) slots[i] = kv->slots[i];
+    return APEX_OK;
+}
+
+apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t *n_items, int32_t *n_merges) {
+    if (!kv || !kv->have_step) return fail(APEX_EINVAL, "no step allocated");
+    if (n_items) *n_items = (int32_t)kv->items.size();
+    if (n_merges) *n_merges = (int32_t)kv->merges.size();
+    if (items)
+        for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)kv->items.size()); ++i) {
+            const WorkItem &w = kv->items[i];
+            int32_t *o = items + 6 * (size_t)i;
+            o[0] = w.b; o[1] = w.g; o[2] = w.blk0; o[3] = w.nblk; o[4] = w.part; o[5] = w.seq;
+        }
+    return APEX_OK;
+}
+
+// Split-KV planner (FlashDecoding lineage): cut each (batch row, kv head)
+// pair into near-equal pieces of whole blocks so the persistent grid sees ~16
+// items per CTA, then order items longest-first (stable) for the dynamic queue.
+static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
+    const int32_t Hkv = kv->d.num_kv_heads, B = (int32_t)lens.size();
+    const int32_t P = kv->grid_override > 0 ? kv->grid_override
+                                            : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count);
+    int64_t T = 0;
+    for (int32_t L : lens) T += cdiv(L, kv->d.block_size) * Hkv;
+    int64_t chunk = kv->forced_chunk_blocks > 0 ? kv->forced_chunk_blocks
+                                                : std::max<int64_t>(4, cdiv(T, 16LL * std::max(P, 1)));
+    std::vector<WorkItem> items;
+    std::vector<MergeItem> merges;
+    int32_t parts = 0;
+    for (int32_t b = 0; b < B; ++b) {
+        const int32_t nblk = (int32_t)cdiv(lens[b], kv->d.block_size);
+        const int32_t nsplit = (int32_t)cdiv(nblk, chunk);
+        for (int32_t g = 0; g < Hkv; ++g) {
+            if (nsplit > 1) merges.push_back({b, g, parts, nsplit});
+            int32_t blk = 0;
+            for (int32_t i = 0; i < nsplit; ++i) {
+                const int32_t n = nblk / nsplit + (i < nblk % nsplit ? 1 : 0);
+                items.push_back({b, g, blk, n, nsplit > 1 ? parts + i : -1, kv->batch_seq[b], lens[b], 0});
+                blk += n;
+            }
+            if (nsplit > 1) parts += nsplit;
+        }
+    }
+    if ((int64_t)items.size() > kv->ws.max_items)
+        return fail(APEX_EINVAL, "split chunk %lld tokens yields %zu work items > workspace capacity %d",
+                    (long long)chunk * kv->d.block_size, items.size(), kv->ws.max_items);
+    std::stable_sort(items.begin(), items.end(),
+                     [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
+    kv->items.swap(items);
+    kv->merges.swap(merges);
+    return APEX_OK;
+}
+
+apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_new, int32_t n, apex_stream stream) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (!seq_ids || !n_new || n < 1 || n > kv->d.max_batch)
+        return fail(APEX_EINVAL, "batch of %d sequences not in [1, max_batch=%d]", n, kv->d.max_batch);
+    const int32_t bs = kv->d.block_size;
+    // ---- validate everything before touching any state (all-or-nothing)
+    std::vector<char> seen(kv->d.max_seqs, 0);
+    int64_t need = 0, rows = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t s = seq_ids[i], k = n_new[i];
+        if (s < 0 || s >= kv->d.max_seqs) return fail(APEX_EINVAL, "seq id %d out of range", s);
+        if (seen[s]) return fail(APEX_EINVAL, "seq id %d repeated in one alloc", s);
+        seen[s] = 1;
+        if (k < 0) return fail(APEX_EINVAL, "n_new[%d] = %d < 0", i, k);
+        const int64_t L = kv->seqs[s].live ? kv->seqs[s].len : 0;
+        if (L + k < 1) return fail(APEX_EINVAL, "seq %d would have an empty context (reading c4)", s);
+        if (L + k > (int64_t)kv->d.max_blocks_per_seq * bs)
+            return fail(APEX_EINVAL, "seq %d would exceed max context %d", s, kv->d.max_blocks_per_seq * bs);
+        need += cdiv(L + k, bs) - cdiv(L, bs);
+        rows += k;
+    }
+    if (rows > kv->d.max_new_tokens)
+        return fail(APEX_EINVAL, "%lld new tokens > max_new_tokens %d", (long long)rows, kv->d.max_new_tokens);
+    if (need > (int64_t)kv->free_stack.size())
+        return fail(APEX_ENOBLOCKS, "need %lld blocks, %zu free", (long long)need, kv->free_stack.size());
+
+    // ---- commit: pop blocks, compute slots and deltas
+    std::vector<int32_t> slots;
+    slots.reserve(rows);
+    std::vector<int2> bt_delta, len_delta;
+    std::vector<int32_t> lens(n);
+    kv->batch_seq.assign(seq_ids, seq_ids + n);
+    for (int32_t i = 0; i < n; ++i) {
+        auto &sq = kv->seqs[seq_ids[i]];
+        if (!sq.live) {
+            sq.live = true;
+            sq.len = 0;
+            sq.blocks.clear();
+        }
+        for (int32_t pos = sq.len; pos < sq.len + n_new[i]; ++pos) {
+            if (pos % bs == 0) {
+                const int32_t blk = kv->free_stack.back();
+                kv->free_stack.pop_back();
+                bt_delta.push_back({seq_ids[i] * kv->d.max_blocks_per_seq + pos / bs, blk});
+                sq.blocks.push_back(blk);
+            }
+            slots.push_back(sq.blocks[pos / bs] * bs + pos % bs);
+        }
+        sq.len += n_new[i];
+        lens[i] = sq.len;
+        len_delta.push_back({seq_ids[i], sq.len});
+    }
+    kv->slots.swap(slots);
+    kv->batch = n;
+    kv->n_rows = (int32_t)rows;
+    kv->have_step = true;
+    apex_status st = plan_step(kv, lens);
+    if (st != APEX_OK) {
+        kv->have_step = false;   // blocks stay allocated (state is consistent); the step is unusable
+        return st;
+    }
+    if (kv->host_only) return APEX_OK;
+
+    // ---- pack the step metadata into pinned staging and upload it
+    const int r = kv->ring;
+    kv->ring ^= 1;
+    if (kv->staged_pending[r]) {
+        cudaError_t e = cudaEventSynchronize(kv->staged[r]);   // its previous H2D must be done
+        if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: staging reuse");
+        kv->staged_pending[r] = false;
+    }
+    uint8_t *host = kv->staging[r];
+    size_t off = 0;
+    auto put = [&](const void *src, size_t bytes) {
+        const size_t at = off;
+        if (bytes) std::memcpy(host + at, src, bytes);
+        off = align_up(off + bytes, 256);
+        return at;
+    };
+    const size_t o_items = put(kv->items.data(), sizeof(WorkItem) * kv->items.size());
+    const size_t o_merges = put(kv->merges.data(), sizeof(MergeItem) * kv->merges.size());
+    const size_t o_slots = put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
+    const size_t o_bt = put(bt_delta.data(), sizeof(int2) * bt_delta.size());
+    const size_t o_len = put(len_delta.data(), sizeof(int2) * len_delta.size());
+    uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
+    if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: metadata upload");
+    kv->staged_pending[r] = true;
+    kv->d_items = (const WorkItem *)(dev + o_items);
+    kv->d_merges = (const MergeItem *)(dev + o_merges);
+    kv->d_slots = (const int32_t *)(dev + o_slots);
+    e = apex::launch_apply_deltas((const int2 *)(dev + o_bt), (int)bt_delta.size(), (const int2 *)(dev + o_len),
+                                  (int)len_delta.size(), kv->d.block_table, kv->d.seq_lens, s);
+    if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: apply deltas");
+    return APEX_OK;
+}
+
+apex_status apex_kv_release(apex_kv *kv, int32_t seq_id) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (seq_id < 0 || seq_id >= kv->d.max_seqs || !kv->seqs[seq_id].live)
+        return fail(APEX_ESEQ, "sequence %d is not live", seq_id);
+    auto &sq = kv->seqs[seq_id];
+    for (auto it = sq.blocks.rbegin(); it != sq.blocks.rend(); ++it) kv->free_stack.push_back(*it);
+    sq = apex_kv::Seq();
+    return APEX_OK;
+}
+
+apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const void *v_new, apex_stream stream) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
+    if (!kv->have_step) return fail(APEX_EINVAL, "apex_kv_append before apex_kv_alloc");
+    if (layer < 0 || layer >= kv->d.num_layers) return fail(APEX_EINVAL, "layer %d out of range", layer);
+    if (kv->n_rows == 0) return APEX_OK;
+    if (!k_new || !v_new) return fail(APEX_EINVAL, "k_new/v_new is NULL");
+    if (((uintptr_t)k_new | (uintptr_t)v_new) & 15) return fail(APEX_EINVAL, "k_new/v_new not 16-byte aligned");
+    cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->k_pools[layer], kv->v_pools[layer],
+                                        kv->d_slots, kv->n_rows, kv->d.num_kv_heads, (cudaStream_t)stream);
+    return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_kv_append");
+}
+
+apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out, float scale,
+                                  apex_stream stream) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
+    if (!kv->have_step) return fail(APEX_EINVAL, "apex_decode_attention before apex_kv_alloc");
+    if (layer < 0 || layer >= kv->d.num_layers) return fail(APEX_EINVAL, "layer %d out of range", layer);
+    if (!q || !out) return fail(APEX_EINVAL, "q/out is NULL");
+    if (((uintptr_t)q | (uintptr_t)out) & 15) return fail(APEX_EINVAL, "q/out not 16-byte aligned");
+    if (!(scale > 0.0f) || !std::isfinite(scale)) return fail(APEX_EINVAL, "scale must be finite and > 0");
+    apex::DecodeParams p{};
+    p.q = q;
+    p.out = out;
+    p.block_table = kv->d.block_table;
+    p.items = kv->d_items;
+    p.merges = kv->d_merges;
+    uint8_t *ws = (uint8_t *)kv->d.workspace;
+    p.part_o = (float *)(ws + kv->ws.part_o);
+    p.part_ml = (float *)(ws + kv->ws.part_ml);
+    p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
+    p.n_items = (int32_t)kv->items.size();
+    p.n_merges = (int32_t)kv->merges.size();
+    p.max_blocks_per_seq = kv->d.max_blocks_per_seq;
+    p.num_q_heads = kv->d.num_q_heads;
+    p.num_kv_heads = kv->d.num_kv_heads;
+    p.scale_log2 = (float)((double)scale * 1.4426950408889634);   // log2(e)
+    p.tma_segs = kv->tma_segs;
+    const int grid = std::min<int>(p.n_items, apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
+    cudaError_t e = apex::launch_decode(kv->d.dtype, kv->group, kv->tmaps[layer], p, grid, (cudaStream_t)stream);
+    return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_decode_attention");
+}
+
+// ---------------------------------------------------------------- cost model
+
+}  // extern "C"
+
+struct apex_cost {
+    std::vector<double> batch, kv, us;   // us[i * nk + j]
+};
+
+namespace {
+// (cell, fraction) of x on a strictly increasing grid, clamped to its ends
+void locate(const std::vector<double> &g, double x, size_t &i, double &f) {
+    if (g.size() == 1 || x <= g.front()) { i = 0; f = 0.0; return; }
+    if (x >= g.back()) { i = g.size() - 2; f = 1.0; return; }
+    i = (size_t)(std::upper_bound(g.begin(), g.end(), x) - g.begin()) - 1;
+    f = (x - g[i]) / (g[i + 1] - g[i]);
+}
+}  // namespace
+
+extern "C" {
+
+apex_status apex_cost_create(const int32_t *batch, int32_t nb, const int64_t *kv_tokens, int32_t nk,
+                             const double *us, apex_cost **out) {
+    if (!out) return fail(APEX_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!batch || !kv_tokens || !us || nb < 1 || nk < 1) return fail(APEX_EINVAL, "empty cost table");
+    for (int32_t i = 0; i < nb; ++i)
+        if (batch[i] <= 0 || (i && batch[i] <= batch[i - 1]))
+            return fail(APEX_EINVAL, "batch grid must be positive and strictly increasing (entry %d)", i);
+    for (int32_t j = 0; j < nk; ++j)
+        if (kv_tokens[j] <= 0 || (j && kv_tokens[j] <= kv_tokens[j - 1]))
+            return fail(APEX_EINVAL, "kv_tokens grid must be positive and strictly increasing (entry %d)", j);
+    for (int64_t i = 0; i < (int64_t)nb * nk; ++i)
+        if (!std::isfinite(us[i]) || us[i] <= 0.0) return fail(APEX_EINVAL, "time entry %lld not finite/positive", (long long)i);
+    apex_cost *c = new (std::nothrow) apex_cost();
+    if (!c) return fail(APEX_EINVAL, "out of host memory");
+    c->batch.assign(batch, batch + nb);
+    c->kv.assign(kv_tokens, kv_tokens + nk);
+    c->us.assign(us, us + (size_t)nb * nk);
+    *out = c;
+    return APEX_OK;
+}
+
+apex_status apex_predict_time(const apex_cost *c, int32_t batch, int64_t kv_tokens, double *us_out) {
+    if (!c || !us_out) return fail(APEX_EINVAL, "cost/us_out is NULL");
+    size_t i, j;
+    double fx, fy;
+    locate(c->batch, (double)batch, i, fx);
+    locate(c->kv, (double)kv_tokens, j, fy);
+    const size_t nk = c->kv.size();
+    const size_t i1 = std::min(i + 1, c->batch.size() - 1), j1 = std::min(j + 1, nk - 1);
+    const double u00 = c->us[i * nk + j], u10 = c->us[i1 * nk + j];
+    const double u01 = c->us[i * nk + j1], u11 = c->us[i1 * nk + j1];
+    *us_out = (1 - fx) * (1 - fy) * u00 + fx * (1 - fy) * u10 + (1 - fx) * fy * u01 + fx * fy * u11;
+    return APEX_OK;
+}
+
+void apex_cost_destroy(apex_cost *c) { delete c; }
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Internal interface between the host core (apex_host.cpp) and the CUDA
+// launchers (append.cu, decode.cu, synth.cu).  Not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/apex.h"
+
+namespace apex {
+
+constexpr int kBlock = 16;          // tokens per KV block (reading c9)
+constexpr int kHeadDim = 128;       // D
+constexpr int kMaxLayers = 64;
+
+// One split-KV work item: the tokens of logical blocks [blk0, blk0+nblk) of
+// (batch row b, kv head g).  32 bytes, read once per item by the decode kernel.
+struct __align__(16) WorkItem {
+    int32_t b;        // batch row (q/out row)
+    int32_t g;        // kv head
+    int32_t blk0;     // first logical block
+    int32_t nblk;     // blocks in this item (>= 1)
+    int32_t part;     // partial slot, or -1 if the item covers the whole (b, g) pair
+    int32_t seq;      // sequence id (block_table row)
+    int32_t len;      // tokens of the sequence (masking of the last block)
+    int32_t pad;
+};
+
+// One (b, g) pair whose items were split: partial slots [part0, part0+nparts).
+struct __align__(16) MergeItem {
+    int32_t b, g, part0, nparts;
+};
+
+struct DecodeParams {
+    const void *q;             // [B][Hq][D]
+    void *out;                 // [B][Hq][D]
+    const int32_t *block_table;
+    const WorkItem *items;
+    const MergeItem *merges;
+    float *part_o;             // [slots][G][D]   unnormalised sum_t p_t v_t (fp32)
+    float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)
+    int32_t *counters;         // [2]: work-queue head, CTAs done
+    int32_t n_items;
+    int32_t n_merges;
+    int32_t max_blocks_per_seq;
+    int32_t num_q_heads;
+    int32_t num_kv_heads;
+    float scale_log2;          // scale * log2(e)
+    int32_t tma_segs;          // 1: one 3-D TMA op per tile; n: n 2-D ops (one per 128-B segment)
+};
+
+struct TmaPair {
+    CUtensorMap k;             // 64-byte aligned opaque descriptors
+    CUtensorMap v;
+};
+
+// launchers: return cudaSuccess or the launch error
+cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
+                                int32_t *block_table, int32_t *seq_lens, cudaStream_t s);
+cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool,
+                          void *v_pool, const int32_t *slots, int n_rows, int n_kv_heads,
+                          cudaStream_t s);
+cudaError_t launch_decode(apex_dtype dt, int group, const TmaPair &tm, const DecodeParams &p,
+                          int grid, cudaStream_t s);
+// persistent-grid size the decode kernel of (dtype, group) runs with on this device
+int decode_grid_ctas(apex_dtype dt, int group, int sm_count);
+bool decode_supported(apex_dtype dt, int group);
+// bytes of dynamic shared memory the decode kernel needs (for attribute setup)
+cudaError_t decode_prepare(apex_dtype dt, int group);
+
+}  // namespace apex

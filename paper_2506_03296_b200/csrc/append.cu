@@ -1,0 +1,76 @@
+// KV append (one K and one V vector per token per layer) and the
+// per-step block-table / length delta application (P:156 dynamic KV management).
+//
+// append: one thread per 16-byte chunk of a (row, head) vector; 128-bit loads
+// and stores.  Pool layout [num_blocks][Hkv][16][D]: a (block, head) tile is
+// contiguous, so the 16 tokens of a block share a 4 KiB (16-bit) / 8 KiB (fp32)
+// tile that the decode kernel fetches with one TMA.  Pure bit copy.
+#include "apex_internal.h"
+
+namespace apex {
+namespace {
+
+__global__ void __launch_bounds__(256) apex_append_kernel(const uint4 *__restrict__ k_new,
+                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_pool,
+                                                          uint4 *__restrict__ v_pool,
+                                                          const int32_t *__restrict__ slots, int n_rows, int hkv,
+                                                          int chunks_per_vec) {
+    const int64_t per_tensor = (int64_t)n_rows * hkv * chunks_per_vec;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * per_tensor; i += stride) {
+        const bool is_v = i >= per_tensor;
+        const int64_t j = is_v ? i - per_tensor : i;
+        const int c = (int)(j % chunks_per_vec);
+        const int64_t rh = j / chunks_per_vec;
+        const int h = (int)(rh % hkv);
+        const int64_t row = rh / hkv;
+        const int32_t slot = __ldg(slots + row);
+        const int64_t blk = slot / kBlock, t = slot % kBlock;
+        const int64_t dst = ((blk * hkv + h) * kBlock + t) * chunks_per_vec + c;
+        if (is_v)
+            v_pool[dst] = __ldg(v_new + j);
+        else
+            k_pool[dst] = __ldg(k_new + j);
+    }
+}
+
+__global__ void apex_apply_deltas_kernel(const int2 *__restrict__ bt_delta, int n_bt,
+                                         const int2 *__restrict__ len_delta, int n_len,
+                                         int32_t *__restrict__ block_table, int32_t *__restrict__ seq_lens) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_bt + n_len; i += gridDim.x * blockDim.x) {
+        if (i < n_bt) {
+            const int2 d = bt_delta[i];
+            block_table[d.x] = d.y;
+        } else {
+            const int2 d = len_delta[i - n_bt];
+            seq_lens[d.x] = d.y;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
+                                int32_t *block_table, int32_t *seq_lens, cudaStream_t s) {
+    const int n = n_bt + n_len;
+    if (n == 0) return cudaSuccess;
+    const int blocks = (n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024;
+    apex_apply_deltas_kernel<<<blocks, 256, 0, s>>>(bt_delta, n_bt, len_delta, n_len, block_table, seq_lens);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                          const int32_t *slots, int n_rows, int n_kv_heads, cudaStream_t s) {
+    if (n_rows <= 0) return cudaSuccess;
+    const int es = dt == APEX_F32 ? 4 : 2;
+    const int cpv = kHeadDim * es / 16;
+    const int64_t total = 2LL * n_rows * n_kv_heads * cpv;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    apex_append_kernel<<<(int)blocks, 256, 0, s>>>(static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new),
+                                                   static_cast<uint4 *>(k_pool), static_cast<uint4 *>(v_pool), slots,
+                                                   n_rows, n_kv_heads, cpv);
+    return cudaGetLastError();
+}
+
+}  // namespace apex

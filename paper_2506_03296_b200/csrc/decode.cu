@@ -1,0 +1,660 @@
+// Split-KV paged decode attention for sm_100a (B200).
+//
+// Computes, per work item (batch row b, kv head g, logical blocks [blk0, blk0+nblk)),
+// the online-softmax partial of  softmax(scale * q . K^T) . V  for the g-th
+// q-group (PAPER.md P:49-53 decode attention, P:51 GQA sharing, P:79
+// memory-bound; FlashDecoding-style split + log-sum-exp merge, cited at P:53).
+//
+// Kernel design:
+//  * persistent grid, 2 CTAs/SM, items pulled longest-first from a device
+//    work queue (atomicAdd), so ragged contexts balance across the 148 SMs;
+//  * warp 0 = producer: reads the block table 32 entries at a time and issues
+//    one TMA (cp.async.bulk.tensor, 128-B swizzle) per K and per V tile of a
+//    (block, kv-head) -- a contiguous 4 KiB (16-bit) / 8 KiB (fp32) tile --
+//    into a STAGES-deep mbarrier ring;
+//  * warps 1..4 = consumers: tile j of an item goes to consumer j % 4, each
+//    keeps its own running (m, l, O) and the four are merged through shared
+//    memory at the item's end (fixed order => deterministic);
+//  * GQA (g >= 2, 16-bit): S = Q_g K^T and O += P V on tensor cores with
+//    mma.sync.m16n8k16 (q-group rows padded to 16; P re-used from the S
+//    accumulator registers as the A operand), K/V fragments via ldmatrix on the
+//    swizzled tiles (conflict-free);
+//  * MHA (g == 1) and fp32: CUDA-core FMAs, one lane per token for q.K
+//    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
+//  * softmax in the log2 domain (scale*log2e folded into S); split items write
+//    (m, l, unnormalised O) fp32 partials that merge_kernel combines in split
+//    order.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "apex_internal.h"
+
+namespace apex {
+namespace {
+
+constexpr int NC = 4;                    // consumer warps
+constexpr int NTHREADS = 32 * (NC + 1);
+constexpr int IR = 4;                    // item-ring entries
+constexpr int CTAS_PER_SM = 2;
+constexpr int kTileRows = kBlock;        // 16 tokens per tile
+
+struct ItemSlot {
+    WorkItem it;
+    int32_t base;      // ring sequence number of the item's first tile
+    int32_t pad[3];
+};
+
+constexpr int kSmemPerCta = 112640;      // 2 CTAs per SM fit the 228 KB SM carve-out
+
+template <int DT, int G> struct Cfg {
+    static constexpr int ES = DT == APEX_F32 ? 4 : 2;
+    static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of one K (or V) tile
+    static constexpr int CB_O = NC * G * kHeadDim * 4;       // per-warp O for the item merge
+    static constexpr int CB_ML = NC * G * 2 * 4;
+    static constexpr int RING = IR * (int)sizeof(ItemSlot);
+    static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
+    static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
+    static constexpr int STAGES = S0 > 12 ? 12 : S0;
+    static constexpr int TILES = STAGES * 2 * TILE;
+    static constexpr int BARS = (2 * STAGES + 2 * IR) * 8;
+    static constexpr int TOTAL = TILES + BARS + RING + CB_O + CB_ML + 1024;   // + alignment slack
+    static_assert(TOTAL <= kSmemPerCta, "shared memory budget");
+    static_assert(STAGES >= 4, "ring too shallow");
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// exp2(x - m) that is exactly 1 when x == m (ctx=1 and max-token bit-exactness)
+__device__ __forceinline__ float ex2_diff(float x, float m) { return x == m ? 1.0f : ex2(x - m); }
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D = A(16x16, rows 8..15 zero) * B(16x8) + D, fp32 accumulate
+template <int DT>
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    const uint32_t z = 0;
+    if constexpr (DT == APEX_BF16)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(z), "r"(a2), "r"(z), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(z), "r"(a2), "r"(z), "r"(b0), "r"(b1));
+}
+
+// 16-bit pair <-> floats
+template <int DT> __device__ __forceinline__ float2 unpack2(uint32_t u) {
+    if constexpr (DT == APEX_BF16) {
+        return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+    } else {
+        __half2 h = *reinterpret_cast<__half2 *>(&u);
+        return __half22float2(h);
+    }
+}
+template <int DT> __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    if constexpr (DT == APEX_BF16) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t *>(&v);
+    } else {
+        __half2 v = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t *>(&v);
+    }
+}
+template <int DT> __device__ __forceinline__ void store4(void *out, size_t idx, float a, float b, float c, float d) {
+    if constexpr (DT == APEX_F32) {
+        *reinterpret_cast<float4 *>(static_cast<float *>(out) + idx) = make_float4(a, b, c, d);
+    } else {
+        uint2 v = make_uint2(pack2<DT>(a, b), pack2<DT>(c, d));
+        *reinterpret_cast<uint2 *>(static_cast<uint16_t *>(out) + idx) = v;
+    }
+}
+
+// ------------------------------------------------------------------ consumers
+// Running online-softmax state of one consumer warp for its share of an item.
+// MMA layout: row = lane/4 (q head of the group), 2 columns per n-tile.
+template <int DT, int G> struct MmaConsumer {
+    uint32_t qa[8][2];          // A fragments of Q (rows >= G zero), per k-step: a0, a2
+    float o[16][4];             // O accumulators, n-tile nd covers dims nd*8..nd*8+7
+    float m, l;                 // running max (log2 units) and this thread's partial sum
+
+    __device__ __forceinline__ void begin(const void *q, const DecodeParams &p, const WorkItem &it, int lane) {
+        const int row = lane >> 2, tid = lane & 3;
+        const uint32_t *qrow = reinterpret_cast<const uint32_t *>(
+            static_cast<const uint16_t *>(q) + ((size_t)it.b * p.num_q_heads + (size_t)it.g * G + row) * kHeadDim);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qa[kk][0] = row < G ? __ldg(qrow + kk * 8 + tid) : 0u;
+            qa[kk][1] = row < G ? __ldg(qrow + kk * 8 + 4 + tid) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+        m = -INFINITY;
+        l = 0.f;
+    }
+
+    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float scale_log2, int lane) {
+        const int r8 = lane & 7, mi = lane >> 3, tid = lane & 3, row = lane >> 2;
+        // ---- S = Q K^T  (16 x 16 tokens), k-steps over d
+        float s[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+        const uint32_t k_lane = kt + (uint32_t)(((mi >> 1) * 8 + r8) * 128);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int c = (kk & 3) * 2 + (mi & 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(k_lane + (kk >> 2) * 2048 + ((c ^ r8) << 4), b0, b1, b2, b3);
+            mma_16816<DT>(s[0], qa[kk][0], qa[kk][1], b0, b1);
+            mma_16816<DT>(s[1], qa[kk][0], qa[kk][1], b2, b3);
+        }
+        // ---- online softmax over this tile's 16 tokens (row = lane/4)
+        float x[4];
+        x[0] = (tid * 2 < valid) ? s[0][0] * scale_log2 : -INFINITY;
+        x[1] = (tid * 2 + 1 < valid) ? s[0][1] * scale_log2 : -INFINITY;
+        x[2] = (8 + tid * 2 < valid) ? s[1][0] * scale_log2 : -INFINITY;
+        x[3] = (8 + tid * 2 + 1 < valid) ? s[1][1] * scale_log2 : -INFINITY;
+        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m, mx);
+        const float alpha = ex2_diff(m, m_new);
+        m = m_new;
+        uint32_t a0 = pack2<DT>(ex2_diff(x[0], m_new), ex2_diff(x[1], m_new));
+        uint32_t a2 = pack2<DT>(ex2_diff(x[2], m_new), ex2_diff(x[3], m_new));
+        if (row >= G) a0 = a2 = 0u;   // padded q rows contribute nothing
+        // l accumulates the same (rounded) p that feeds the P.V product
+        const float2 p01 = unpack2<DT>(a0), p23 = unpack2<DT>(a2);
+        l = l * alpha + ((p01.x + p01.y) + (p23.x + p23.y));
+#pragma unroll
+        for (int nd = 0; nd < 16; ++nd) {
+            o[nd][0] *= alpha;
+            o[nd][1] *= alpha;
+        }
+        // ---- O += P V: V fragments via ldmatrix.trans; masked rows zeroed (NaN-safe)
+        uint32_t mlo = 0xffffffffu, mhi = 0xffffffffu;
+        if (valid < kTileRows) {
+            mlo = (tid * 2 < valid ? 0x0000ffffu : 0u) | (tid * 2 + 1 < valid ? 0xffff0000u : 0u);
+            mhi = (8 + tid * 2 < valid ? 0x0000ffffu : 0u) | (8 + tid * 2 + 1 < valid ? 0xffff0000u : 0u);
+        }
+        const uint32_t v_lane = vt + (uint32_t)(((mi & 1) * 8 + r8) * 128);
+#pragma unroll
+        for (int nd = 0; nd < 16; nd += 2) {
+            const int c = (nd & 7) + (mi >> 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(v_lane + (nd >> 3) * 2048 + ((c ^ r8) << 4), b0, b1, b2, b3);
+            mma_16816<DT>(o[nd], a0, a2, b0 & mlo, b1 & mhi);
+            mma_16816<DT>(o[nd + 1], a0, a2, b2 & mlo, b3 & mhi);
+        }
+    }
+
+    __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        const int row = lane >> 2, tid = lane & 3;
+        if (row < G) {
+            float *dst = cb_o + ((size_t)wc * G + row) * kHeadDim;
+#pragma unroll
+            for (int nd = 0; nd < 16; ++nd)
+                *reinterpret_cast<float2 *>(dst + nd * 8 + tid * 2) = make_float2(o[nd][0], o[nd][1]);
+            if (tid == 0) {
+                cb_m[wc * G + row] = m;
+                cb_l[wc * G + row] = l;
+            }
+        }
+    }
+};
+
+// CUDA-core consumer for g == 1 (fp32 or 16-bit).  q.K: lane t (0..15) owns token
+// t, half hh = lane/16 owns dims hh*64..hh*64+63.  P.V: lane owns 8 (16-bit) or
+// 4 (fp32) dims; 16-bit lanes split even/odd tokens by half-warp.
+template <int DT> struct SimtConsumer {
+    static constexpr bool F32 = DT == APEX_F32;
+    float qv[64];               // q * scale*log2e, dims hh*64 ..
+    float o[8];                 // 16-bit: 8 dims; fp32: 4 dims (o[0..3])
+    float m, l;                 // l: per-lane partial of sum p (lanes 0..15 distinct)
+
+    __device__ __forceinline__ void begin(const void *q, const DecodeParams &p, const WorkItem &it, int lane) {
+        const int hh = lane >> 4;
+        const size_t base = ((size_t)it.b * p.num_q_heads + it.g) * kHeadDim + hh * 64;
+        if constexpr (F32) {
+            const float4 *src = reinterpret_cast<const float4 *>(static_cast<const float *>(q) + base);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                float4 v = __ldg(src + i);
+                qv[4 * i] = v.x * p.scale_log2;
+                qv[4 * i + 1] = v.y * p.scale_log2;
+                qv[4 * i + 2] = v.z * p.scale_log2;
+                qv[4 * i + 3] = v.w * p.scale_log2;
+            }
+        } else {
+            const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(q) + base);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint4 v = __ldg(src + i);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float2 f = unpack2<DT>(w[j]);
+                    qv[8 * i + 2 * j] = f.x * p.scale_log2;
+                    qv[8 * i + 2 * j + 1] = f.y * p.scale_log2;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        m = -INFINITY;
+        l = 0.f;
+    }
+
+    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float, int lane) {
+        const int t = lane & 15, hh = lane >> 4, t7 = t & 7;
+        // ---- s_t (log2 units): lane t, dims of half hh
+        float acc = 0.f;
+        if constexpr (F32) {
+#pragma unroll
+            for (int sg = 0; sg < 2; ++sg) {
+                const uint32_t rowa = kt + (uint32_t)((2 * hh + sg) * 2048 + t * 128);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint4 k4 = lds128(rowa + ((c ^ t7) << 4));
+                    const float *qq = qv + sg * 32 + c * 4;
+                    acc = fmaf(qq[0], __uint_as_float(k4.x), acc);
+                    acc = fmaf(qq[1], __uint_as_float(k4.y), acc);
+                    acc = fmaf(qq[2], __uint_as_float(k4.z), acc);
+                    acc = fmaf(qq[3], __uint_as_float(k4.w), acc);
+                }
+            }
+        } else {
+            const uint32_t rowa = kt + (uint32_t)(hh * 2048 + t * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint4 k4 = lds128(rowa + ((c ^ t7) << 4));
+                const uint32_t w[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float2 f = unpack2<DT>(w[j]);
+                    acc = fmaf(qv[c * 8 + 2 * j], f.x, acc);
+                    acc = fmaf(qv[c * 8 + 2 * j + 1], f.y, acc);
+                }
+            }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        const float x = t < valid ? acc : -INFINITY;
+        float mx = x;
+#pragma unroll
+        for (int w = 1; w < 16; w <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, w));
+        const float m_new = fmaxf(m, mx);
+        const float alpha = ex2_diff(m, m_new);
+        m = m_new;
+        const float pt = ex2_diff(x, m_new);
+        l = l * alpha + pt;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] *= alpha;
+        // ---- O += p_r V_r over lane-owned dims
+        if constexpr (F32) {
+            const int sg = lane >> 3, c = lane & 7;
+#pragma unroll 4
+            for (int r = 0; r < kTileRows; ++r) {
+                const float pr = __shfl_sync(0xffffffffu, pt, r);
+                if (r < valid) {
+                    uint4 v4 = lds128(vt + (uint32_t)(sg * 2048 + r * 128) + ((c ^ (r & 7)) << 4));
+                    o[0] = fmaf(pr, __uint_as_float(v4.x), o[0]);
+                    o[1] = fmaf(pr, __uint_as_float(v4.y), o[1]);
+                    o[2] = fmaf(pr, __uint_as_float(v4.z), o[2]);
+                    o[3] = fmaf(pr, __uint_as_float(v4.w), o[3]);
+                }
+            }
+        } else {
+            const int sg = (lane & 15) >> 3, c = lane & 7;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = 2 * i + hh;
+                const float pr = __shfl_sync(0xffffffffu, pt, r);
+                if (r < valid) {
+                    uint4 v4 = lds128(vt + (uint32_t)(sg * 2048 + r * 128) + ((c ^ (r & 7)) << 4));
+                    const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float2 f = unpack2<DT>(w[j]);
+                        o[2 * j] = fmaf(pr, f.x, o[2 * j]);
+                        o[2 * j + 1] = fmaf(pr, f.y, o[2 * j + 1]);
+                    }
+                }
+            }
+        }
+    }
+
+    __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
+#pragma unroll
+        for (int w = 1; w < 16; w <<= 1) l += __shfl_xor_sync(0xffffffffu, l, w);
+        float *dst = cb_o + (size_t)wc * kHeadDim;
+        if constexpr (F32) {
+            const int sg = lane >> 3, c = lane & 7;
+            *reinterpret_cast<float4 *>(dst + sg * 32 + c * 4) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(0xffffffffu, o[i], 16);
+            if (lane < 16) {
+                const int sg = lane >> 3, c = lane & 7;
+                *reinterpret_cast<float4 *>(dst + sg * 64 + c * 8) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4 *>(dst + sg * 64 + c * 8 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+            }
+        }
+        if (lane == 0) {
+            cb_m[wc] = m;
+            cb_l[wc] = l;
+        }
+    }
+};
+
+template <int DT, int G> struct ConsumerSel { using T = MmaConsumer<DT, G>; };
+template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
+
+// ------------------------------------------------------------------ decode kernel
+template <int DT, int G>
+__global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
+    apex_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                       const DecodeParams p) {
+    using C = Cfg<DT, G>;
+    using S = C;
+    constexpr int STAGES = C::STAGES, TILE = C::TILE;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::TILES);
+    ItemSlot *ring = reinterpret_cast<ItemSlot *>(smem + S::TILES + S::BARS);
+    float *cb_o = reinterpret_cast<float *>(smem + S::TILES + S::BARS + S::RING);
+    float *cb_m = cb_o + NC * G * kHeadDim;
+    float *cb_l = cb_m + NC * G;
+    const uint32_t tiles_u = smem_u32(smem);
+    const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES;
+    const uint32_t ifull0 = empty0 + 8 * STAGES, iempty0 = ifull0 + 8 * IR;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);
+        }
+        for (int i = 0; i < IR; ++i) {
+            mbar_init(ifull0 + 8 * i, 1);
+            mbar_init(iempty0 + 8 * i, NC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ================= producer: work queue + block table + TMA =================
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+        }
+        int32_t issued = 0;
+        for (int k = 0;; ++k) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.counters, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            const int slot = k % IR, use = k / IR;
+            if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
+            __syncwarp();
+            if (idx >= p.n_items) {
+                if (lane == 0) {
+                    ring[slot].it.nblk = 0;   // sentinel: no more items
+                    mbar_arrive(ifull0 + 8 * slot);
+                }
+                break;
+            }
+            const WorkItem it = p.items[idx];
+            if (lane == 0) {
+                ring[slot].it = it;
+                ring[slot].base = issued;
+                mbar_arrive(ifull0 + 8 * slot);
+            }
+            const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
+            for (int j0 = 0; j0 < it.nblk; j0 += 32) {
+                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
+                const int cnt = min(32, it.nblk - j0);
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const int phys = __shfl_sync(0xffffffffu, my, jj);
+                    if (lane == 0) {
+                        const int s = issued % STAGES, u = issued / STAGES;
+                        if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
+                        const uint32_t bar = full0 + 8 * s;
+                        mbar_expect_tx(bar, 2 * TILE);
+                        const int row = (phys * p.num_kv_heads + it.g) * kTileRows;
+                        const uint32_t dk = tiles_u + s * 2 * TILE, dv = dk + TILE;
+                        if (p.tma_segs == 1) {
+                            tma_load_3d(dk, &tmk, bar, 0, row, 0);
+                            tma_load_3d(dv, &tmv, bar, 0, row, 0);
+                        } else {
+                            for (int sg = 0; sg < p.tma_segs; ++sg) {
+                                tma_load_2d(dk + sg * 2048, &tmk, bar, sg * (128 / C::ES), row);
+                                tma_load_2d(dv + sg * 2048, &tmv, bar, sg * (128 / C::ES), row);
+                            }
+                        }
+                    }
+                    ++issued;
+                }
+            }
+        }
+        // last CTA out resets the queue for the next launch on this layer
+        if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(p.counters + 1, 1) == (int)gridDim.x - 1) {
+                atomicExch(p.counters, 0);
+                atomicExch(p.counters + 1, 0);
+            }
+        }
+    } else {
+        // ================= consumers =================
+        const int wc = warp - 1;
+        typename ConsumerSel<DT, G>::T st;
+        for (int k = 0;; ++k) {
+            const int slot = k % IR, use = k / IR;
+            mbar_wait(ifull0 + 8 * slot, use & 1);
+            const WorkItem it = ring[slot].it;
+            const int32_t base = ring[slot].base;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(iempty0 + 8 * slot);
+            if (it.nblk == 0) break;
+            st.begin(p.q, p, it, lane);
+            for (int j = wc; j < it.nblk; j += NC) {
+                const int n = base + j, s = n % STAGES, u = n / STAGES;
+                mbar_wait(full0 + 8 * s, u & 1);
+                const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
+                const uint32_t kt = tiles_u + s * 2 * TILE;
+                st.tile(kt, kt + TILE, valid, p.scale_log2, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty0 + 8 * s);
+            }
+            st.finish(cb_o, cb_m, cb_l, wc, lane);
+            named_bar_sync(1, NC * 32);
+            // ---- merge the NC warp states (fixed order), 4 dims per step
+            for (int idx = threadIdx.x - 32; idx < G * kHeadDim / 4; idx += NC * 32) {
+                const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < NC; ++w) M = fmaxf(M, cb_m[w * G + row]);
+                float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll
+                for (int w = 0; w < NC; ++w) {
+                    const float e = ex2_diff(cb_m[w * G + row], M);
+                    const float4 v = *reinterpret_cast<const float4 *>(cb_o + ((size_t)w * G + row) * kHeadDim + d4);
+                    den = fmaf(e, cb_l[w * G + row], den);
+                    a = fmaf(e, v.x, a);
+                    b = fmaf(e, v.y, b);
+                    c = fmaf(e, v.z, c);
+                    d = fmaf(e, v.w, d);
+                }
+                if (it.part < 0) {
+                    const size_t o = ((size_t)it.b * p.num_q_heads + (size_t)it.g * G + row) * kHeadDim + d4;
+                    store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
+                } else {
+                    const size_t o = ((size_t)it.part * G + row) * kHeadDim + d4;
+                    *reinterpret_cast<float4 *>(p.part_o + o) = make_float4(a, b, c, d);
+                    if (d4 == 0) *reinterpret_cast<float2 *>(p.part_ml + ((size_t)it.part * G + row) * 2) = make_float2(M, den);
+                }
+            }
+            named_bar_sync(1, NC * 32);
+        }
+    }
+}
+
+// log-sum-exp merge of split items (fixed split order): one CTA per (b, g) pair
+template <int DT, int G>
+__global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
+    const MergeItem mg = p.merges[blockIdx.x];
+    for (int idx = threadIdx.x; idx < G * kHeadDim / 4; idx += blockDim.x) {
+        const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+        float M = -INFINITY;
+        for (int i = 0; i < mg.nparts; ++i) M = fmaxf(M, p.part_ml[((size_t)(mg.part0 + i) * G + row) * 2]);
+        float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+        for (int i = 0; i < mg.nparts; ++i) {
+            const size_t pi = (size_t)(mg.part0 + i) * G + row;
+            const float2 ml = *reinterpret_cast<const float2 *>(p.part_ml + pi * 2);
+            const float e = ex2_diff(ml.x, M);
+            const float4 v = *reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4);
+            den = fmaf(e, ml.y, den);
+            a = fmaf(e, v.x, a);
+            b = fmaf(e, v.y, b);
+            c = fmaf(e, v.z, c);
+            d = fmaf(e, v.w, d);
+        }
+        const size_t o = ((size_t)mg.b * p.num_q_heads + (size_t)mg.g * G + row) * kHeadDim + d4;
+        store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
+    }
+}
+
+template <int DT, int G> cudaError_t prepare() {
+    return cudaFuncSetAttribute(apex_decode_kernel<DT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                Cfg<DT, G>::TOTAL);
+}
+
+template <int DT, int G>
+cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
+    if (grid > 0) {
+        apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (p.n_merges > 0) {
+        apex_merge_kernel<DT, G><<<p.n_merges, 128, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+bool decode_supported(apex_dtype dt, int group) {
+    if (dt == APEX_F32) return group == 1;
+    return group == 1 || group == 2 || group == 4 || group == 8;
+}
+
+int decode_grid_ctas(apex_dtype, int, int sm_count) { return CTAS_PER_SM * sm_count; }
+
+cudaError_t decode_prepare(apex_dtype dt, int group) {
+    if (!decode_supported(dt, group)) return cudaErrorInvalidValue;
+    switch (dt) {
+    case APEX_F32: return prepare<APEX_F32, 1>();
+    case APEX_F16:
+        switch (group) {
+        case 1: return prepare<APEX_F16, 1>();
+        case 2: return prepare<APEX_F16, 2>();
+        case 4: return prepare<APEX_F16, 4>();
+        default: return prepare<APEX_F16, 8>();
+        }
+    default:
+        switch (group) {
+        case 2: return prepare<APEX_BF16, 2>();
+        case 4: return prepare<APEX_BF16, 4>();
+        default: return prepare<APEX_BF16, 8>();
+        }
+    }
+}
+
+cudaError_t launch_decode(apex_dtype dt, int group, const TmaPair &tm, const DecodeParams &p, int grid,
+                          cudaStream_t s) {
+    if (!decode_supported(dt, group)) return cudaErrorInvalidValue;
+#define APEX_LAUNCH_ARGS (tm, p, grid, s)
+    switch (dt) {
+    case APEX_F32: return launch<APEX_F32, 1> APEX_LAUNCH_ARGS;
+    case APEX_F16:
+        switch (group) {
+        case 1: return launch<APEX_F16, 1> APEX_LAUNCH_ARGS;
+        case 2: return launch<APEX_F16, 2> APEX_LAUNCH_ARGS;
+        case 4: return launch<APEX_F16, 4> APEX_LAUNCH_ARGS;
+        default: return launch<APEX_F16, 8> APEX_LAUNCH_ARGS;
+        }
+    default:
+        switch (group) {
+        case 2: return launch<APEX_BF16, 2> APEX_LAUNCH_ARGS;
+        case 4: return launch<APEX_BF16, 4> APEX_LAUNCH_ARGS;
+        default: return launch<APEX_BF16, 8> APEX_LAUNCH_ARGS;
+        }
+    }
+#undef APEX_LAUNCH_ARGS
+}
+
+}  // namespace apex

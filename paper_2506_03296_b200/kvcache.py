@@ -1,0 +1,143 @@
+"""PagedKVCache: torch-owned device memory + the C-ABI handle.
+
+PyTorch supplies device memory (pools, block table, lengths, workspace) and the
+current CUDA stream; the allocator, planner, append, decode attention and merge
+all run inside libapex.so (include/apex.h).  A host-only cache (host_only=True)
+runs the allocator/planner without any CUDA call (CPU tests, sharding logic).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import apex as A
+
+_TORCH_DT = {"f32": "float32", "f16": "float16", "bf16": "bfloat16"}
+
+
+def torch_dtype(dtype: str):
+    import torch
+    return getattr(torch, _TORCH_DT[dtype])
+
+
+def _stream_ptr(device) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class PagedKVCache:
+    def __init__(self, *, num_layers: int, num_q_heads: int, num_kv_heads: int, num_blocks: int,
+                 max_seqs: int, max_blocks_per_seq: int, max_batch: int, max_new_tokens: int,
+                 dtype: str = "bf16", head_dim: int = 128, block_size: int = 16, device="cuda",
+                 host_only: bool = False, alloc_pools: bool = True):
+        self.num_layers, self.num_q_heads, self.num_kv_heads = num_layers, num_q_heads, num_kv_heads
+        self.head_dim, self.block_size, self.dtype = head_dim, block_size, dtype
+        self.num_blocks, self.max_seqs, self.max_blocks_per_seq = num_blocks, max_seqs, max_blocks_per_seq
+        self.max_batch, self.max_new_tokens = max_batch, max_new_tokens
+        self.host_only = host_only
+        self.batch_seq_ids: list[int] = []
+        self.n_rows = 0
+        desc = A.apex_kv_desc(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_blocks, max_seqs,
+                              max_blocks_per_seq, max_batch, max_new_tokens, A.DTYPE_CODE[dtype])
+        if host_only:
+            self.device = None
+            self.handle = A.apex_kv_create(desc)
+            return
+        import torch
+        self.device = torch.device(device)
+        tdt = torch_dtype(dtype)
+        shape = (num_blocks, num_kv_heads, block_size, head_dim)
+        self.k_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
+        self.v_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
+        self.block_table = torch.zeros((max_seqs, max_blocks_per_seq), dtype=torch.int32, device=self.device)
+        self.seq_lens = torch.zeros((max_seqs,), dtype=torch.int32, device=self.device)
+        kp = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.k_pools])
+        vp = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.v_pools])
+        desc.k_pool, desc.v_pool = kp, vp
+        desc.block_table, desc.seq_lens = self.block_table.data_ptr(), self.seq_lens.data_ptr()
+        nbytes = A.apex_kv_workspace_bytes(desc)
+        if nbytes == 0:
+            # surface the validation message
+            A.apex_kv_create(desc)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        desc.workspace, desc.workspace_bytes = self.workspace.data_ptr(), nbytes
+        self.handle = A.apex_kv_create(desc)
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "handle", None):
+            A.apex_kv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self) -> int:
+        return 0 if self.host_only else _stream_ptr(self.device)
+
+    # -- step API (names follow the C ABI)
+    def alloc(self, seq_ids, n_new):
+        A.apex_kv_alloc(self.handle, seq_ids, n_new, self._stream())
+        self.batch_seq_ids = [int(s) for s in seq_ids]
+        self.n_rows = int(sum(int(x) for x in n_new))
+
+    def release(self, seq_id: int):
+        A.apex_kv_release(self.handle, seq_id)
+
+    def append(self, layer: int, k_new, v_new):
+        self._check_rows(k_new, self.n_rows, self.num_kv_heads)
+        self._check_rows(v_new, self.n_rows, self.num_kv_heads)
+        A.apex_kv_append(self.handle, layer, k_new.data_ptr(), v_new.data_ptr(), self._stream())
+
+    def decode(self, layer: int, q, out=None, scale: float | None = None):
+        import torch
+        B = len(self.batch_seq_ids)
+        self._check_rows(q, B, self.num_q_heads)
+        if out is None:
+            out = torch.empty_like(q)
+        else:
+            self._check_rows(out, B, self.num_q_heads)
+        if scale is None:
+            scale = 1.0 / math.sqrt(self.head_dim)
+        A.apex_decode_attention(self.handle, layer, q.data_ptr(), out.data_ptr(), scale, self._stream())
+        return out
+
+    def _check_rows(self, t, rows, heads):
+        if t.device != self.device or t.dtype != torch_dtype(self.dtype) or not t.is_contiguous():
+            raise ValueError(f"expected contiguous {self.dtype} tensor on {self.device}, got {t.dtype} on {t.device}")
+        if tuple(t.shape) != (rows, heads, self.head_dim):
+            raise ValueError(f"expected shape {(rows, heads, self.head_dim)}, got {tuple(t.shape)}")
+
+    # -- knobs / introspection
+    def set_split(self, chunk_tokens: int):
+        A.apex_kv_set_split(self.handle, chunk_tokens)
+
+    def set_grid(self, ctas: int):
+        A.apex_kv_set_grid(self.handle, ctas)
+
+    def num_free_blocks(self) -> int:
+        return A.apex_kv_num_free_blocks(self.handle)
+
+    def seq_info(self, seq_id: int):
+        return A.apex_kv_seq_info(self.handle, seq_id)
+
+    def last_slots(self):
+        return A.apex_kv_last_slots(self.handle)
+
+    def plan(self):
+        return A.apex_kv_plan(self.handle)
+
+
+def synth_rows(out, dtype: str, tensor: int, layer: int, row_b, row_pos, head_offset: int = 0, seed: int = 0,
+               amp: float = 1.0):
+    """Fill out [R][H][D] on the GPU with synth.gen_rows-identical values (device twin)."""
+    import torch
+    assert out.is_contiguous() and out.dim() == 3
+    rb = row_b.to(device=out.device, dtype=torch.int32).contiguous()
+    rp = row_pos.to(device=out.device, dtype=torch.int32).contiguous()
+    A.apex_synth_rows(out.data_ptr(), dtype, tensor, layer, rb.data_ptr(), rp.data_ptr(), out.shape[0],
+                      out.shape[1], head_offset, out.shape[2], seed, amp, _stream_ptr(out.device))
+    return out

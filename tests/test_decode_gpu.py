@@ -1,0 +1,173 @@
+"""GPU parity tests through the C ABI (libapex.so) against the float64 oracle.
+
+Small shapes span several tiles, split items and ragged tails; the BASELINE
+configs C1-C5 are covered at full size in test_configs_gpu.py.
+"""
+import numpy as np
+import pytest
+
+import synth
+from helpers import check_close, decode_step, gen_dev, make_cache, oracle_rows, prefill, to_f64
+
+pytestmark = pytest.mark.gpu
+
+COMBOS = [("f32", 4, 4), ("f16", 4, 4), ("f16", 8, 2), ("f16", 16, 4), ("f16", 16, 2), ("bf16", 8, 4),
+          ("bf16", 16, 4), ("bf16", 16, 2)]
+RAGGED = [1, 2, 15, 16, 17, 31, 64, 100, 257, 1000, 2049]
+
+
+def run_case(dtype, hq, hkv, ctx, qamp=1.0, split=None, interleave=0, seed=0, num_blocks=None, poison=False):
+    import torch
+    B = len(ctx)
+    mbps = max(-(-c // 16) for c in ctx) + 1
+    nb = num_blocks or sum(-(-c // 16) for c in ctx) + 8
+    cache = make_cache(dtype, hq, hkv, nb, max_seqs=B + 4, max_blocks_per_seq=mbps)
+    if poison:
+        for t in cache.k_pools + cache.v_pools:
+            t.view(torch.uint8).fill_(0xFF)        # NaN bit patterns in every dtype
+    if split is not None:
+        cache.set_split(split)
+    seqs = list(range(2, 2 + B))
+    prefill(cache, seqs, ctx, seed=seed, interleave=interleave)
+    out = decode_step(cache, seqs, ctx, seed=seed, qamp=qamp)
+    torch.cuda.synchronize()
+    return cache, seqs, to_f64(out, dtype)
+
+
+def test_generator_twin_bitexact(cuda_lib):
+    import torch
+    from paper_2506_03296_b200.kvcache import synth_rows, torch_dtype
+    rng = np.random.default_rng(0)
+    for dtype in ("f32", "f16", "bf16"):
+        for (tensor, layer, heads, hoff, amp) in [(0, 0, 32, 0, 1.0), (1, 5, 8, 3, 1.0), (2, 63, 4, 100, 8.0),
+                                                   (0, 1, 1, 127, 64.0)]:
+            R = 257
+            b = rng.integers(0, 65536, R)
+            pos = rng.integers(0, 1 << 18, R)
+            out = torch.empty((R, heads, 128), dtype=torch_dtype(dtype), device="cuda")
+            synth_rows(out, dtype, tensor, layer, torch.as_tensor(b), torch.as_tensor(pos), head_offset=hoff,
+                       seed=7, amp=amp)
+            host = synth.gen_rows(tensor, layer, b, pos, heads, 128, dtype, seed=7, amp=amp, head_offset=hoff)
+            dev = out.cpu()
+            dev = dev.numpy() if dtype == "f32" else dev.view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(dev, host), (dtype, tensor)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16", "bf16"])
+def test_append_bitexact(cuda_lib, dtype):
+    import torch
+    hkv = 4
+    cache = make_cache(dtype, 4 if dtype == "f32" else 8, hkv, num_blocks=40, max_seqs=8, max_blocks_per_seq=16)
+    ctx = [3, 40, 17, 100]
+    seqs = [0, 3, 5, 6]
+    prefill(cache, seqs, ctx, interleave=7)
+    # every written slot must hold exactly the generator's row (host scatter check)
+    pool_k = cache.k_pools[0].cpu()
+    pool_v = cache.v_pools[0].cpu()
+    for s, c in zip(seqs, ctx):
+        L, blocks = cache.seq_info(s)
+        assert L == c - 1
+        want_k = synth.gen_seq(1, 0, s, L, hkv, 128, dtype)
+        want_v = synth.gen_seq(2, 0, s, L, hkv, 128, dtype)
+        for t in range(L):
+            blk = blocks[t // 16]
+            gk = pool_k[blk, :, t % 16]
+            gv = pool_v[blk, :, t % 16]
+            if dtype != "f32":
+                gk, gv = gk.view(torch.int16).numpy().view(np.uint16), gv.view(torch.int16).numpy().view(np.uint16)
+            else:
+                gk, gv = gk.numpy(), gv.numpy()
+            assert np.array_equal(gk, want_k[t]) and np.array_equal(gv, want_v[t]), (s, t)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", COMBOS)
+def test_decode_ragged_parity(cuda_lib, dtype, hq, hkv):
+    ctx = RAGGED
+    _, seqs, out = run_case(dtype, hq, hkv, ctx, interleave=48)
+    ref = oracle_rows(seqs, ctx, hq, hkv, dtype)
+    check_close(out, ref, dtype)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", [("f32", 4, 4), ("bf16", 16, 4), ("f16", 4, 4)])
+@pytest.mark.parametrize("qamp", [8.0, 64.0])
+def test_decode_peaky_scores(cuda_lib, dtype, hq, hkv, qamp):
+    ctx = [5, 300, 1111]
+    _, seqs, out = run_case(dtype, hq, hkv, ctx, qamp=qamp)
+    ref = oracle_rows(seqs, ctx, hq, hkv, dtype, qamp=qamp)
+    # reading c6: large logits (q x64) use the looser 1e-4 fp32 normwise bound
+    check_close(out, ref, dtype, tol_f32=1e-5 if qamp <= 8 else 1e-4)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", COMBOS)
+def test_ctx1_returns_v0_bitexact(cuda_lib, dtype, hq, hkv):
+    import torch
+    _, seqs, out = run_case(dtype, hq, hkv, [1, 1, 1])
+    g = hq // hkv
+    for i, s in enumerate(seqs):
+        v0 = synth.gen_rows(2, 0, [s], [0], hkv, 128, dtype)[0]
+        v0 = v0.astype(np.float64) if dtype == "f32" else (
+            v0.view(np.float16).astype(np.float64) if dtype == "f16"
+            else (v0.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
+        for h in range(hq):
+            assert np.array_equal(out[i, h], v0[h // g]), (dtype, s, h)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", [("f32", 4, 4), ("f16", 4, 4), ("bf16", 16, 4)])
+def test_nan_poisoned_pools_do_not_leak(cuda_lib, dtype, hq, hkv):
+    ctx = [1, 7, 33, 250]
+    _, _, clean = run_case(dtype, hq, hkv, ctx)
+    _, _, dirty = run_case(dtype, hq, hkv, ctx, poison=True)
+    assert np.isfinite(dirty).all()
+    assert np.array_equal(clean, dirty)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", [("f32", 4, 4), ("bf16", 16, 4), ("f16", 8, 8)])
+def test_block_shuffle_bit_identical(cuda_lib, dtype, hq, hkv):
+    ctx = [77, 500, 1025, 3]
+    _, _, a = run_case(dtype, hq, hkv, ctx, interleave=0, split=128)
+    _, _, b = run_case(dtype, hq, hkv, ctx, interleave=16, split=128, num_blocks=400)
+    _, _, c = run_case(dtype, hq, hkv, ctx, interleave=33, split=128, num_blocks=300)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", [("f32", 4, 4), ("bf16", 16, 4), ("f16", 4, 4)])
+def test_split_invariance(cuda_lib, dtype, hq, hkv):
+    ctx = [1500, 2047, 64]
+    outs = [run_case(dtype, hq, hkv, ctx, split=s)[2] for s in (16, 32, 112, 1024, 4096)]
+    ref = oracle_rows(list(range(2, 5)), ctx, hq, hkv, dtype)
+    for o in outs:
+        check_close(o, ref, dtype)
+        if dtype == "f32":
+            d = np.abs(o - outs[-1]).max(axis=-1) / np.abs(outs[-1]).max(axis=-1)
+            assert d.max() <= 1e-6
+
+
+def test_deterministic_repeat(cuda_lib):
+    import torch
+    cache = make_cache("bf16", 32, 8, num_blocks=2000, max_seqs=8, max_blocks_per_seq=300)
+    ctx = [4000, 123, 2500]
+    seqs = [0, 1, 2]
+    prefill(cache, seqs, ctx)
+    cache.alloc(seqs, [1, 1, 1])
+    k = gen_dev(cache, 1, 0, seqs, [c - 1 for c in ctx], 8)
+    cache.append(0, k, k)
+    q = gen_dev(cache, 0, 0, seqs, [c - 1 for c in ctx], 32)
+    outs = [cache.decode(0, q).clone() for _ in range(5)]
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_errors_and_unsupported(cuda_lib):
+    from paper_2506_03296_b200 import apex as A
+    cache = make_cache("bf16", 16, 4, num_blocks=8, max_seqs=4, max_blocks_per_seq=4)
+    with pytest.raises(A.ApexError) as e:
+        A.apex_decode_attention(cache.handle, 0, 0, 0, 0.1)
+    assert e.value.code == "EINVAL"          # before any alloc
+    cache.alloc([0], [5])
+    with pytest.raises(A.ApexError) as e:
+        A.apex_kv_append(cache.handle, 3, 16, 16)
+    assert e.value.code == "EINVAL"          # bad layer
+    with pytest.raises(A.ApexError) as e:
+        cache.alloc([1], [16 * 8])
+    assert e.value.code in ("ENOBLOCKS", "EINVAL")

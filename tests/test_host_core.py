@@ -1,0 +1,202 @@
+"""Host-core tests through the C ABI (CPU only; host-only handles make no CUDA calls).
+
+* the library loads and exports every function include/*.h declares;
+* allocator: bit-exact block tables / slots / free counts vs oracle/alloc_model.py
+  (independent Python model of reading c10), all-or-nothing errors;
+* planner: every (batch row, kv head, block) covered exactly once, split
+  bookkeeping consistent, longest-first order;
+* cost model: apex_predict_time vs oracle/cost_model.interp, exact at grid
+  points, clamped, loader validation.
+"""
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+from oracle import cost_model as cm
+from oracle.alloc_model import AllocError, AllocModel
+from paper_2506_03296_b200 import apex as A
+from paper_2506_03296_b200 import build as B
+from paper_2506_03296_b200.kvcache import PagedKVCache
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+
+
+def host_cache(**kw):
+    args = dict(num_layers=1, num_q_heads=8, num_kv_heads=2, num_blocks=64, max_seqs=16, max_blocks_per_seq=32,
+                max_batch=16, max_new_tokens=4096, dtype="bf16", host_only=True)
+    args.update(kw)
+    return PagedKVCache(**args)
+
+
+def test_exports_every_declared_symbol():
+    declared = set()
+    for h in ("apex.h", "apex_synth.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        declared |= set(re.findall(r"\b(apex_[a-z0-9_]+)\s*\(", src))
+    nm = subprocess.run(["nm", "-D", "--defined-only", A.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in nm.splitlines() if " T " in line}
+    assert declared and declared <= exported, declared - exported
+    assert declared == set(A.EXPORTS)
+    assert "sm_100a" in A.apex_version()
+
+
+def test_alloc_matches_python_model_random():
+    rnd = random.Random(0)
+    for trial in range(20):
+        nb = rnd.choice([8, 33, 64])
+        c = host_cache(num_blocks=nb)
+        m = AllocModel(nb, 16, 32)
+        for step in range(60):
+            if m.table and rnd.random() < 0.25:
+                sid = rnd.choice(list(m.table))
+                m.release(sid)
+                c.release(sid)
+            else:
+                ids = rnd.sample(range(16), rnd.randint(1, 5))
+                nn = [rnd.choice([0, 1, 1, 1, 15, 16, 17, 40]) for _ in ids]
+                try:
+                    want = m.alloc(ids, nn)
+                    err = None
+                except AllocError as e:
+                    err = e.code
+                if err is None:
+                    c.alloc(ids, nn)
+                    assert c.last_slots() == want
+                else:
+                    with pytest.raises(A.ApexError) as ei:
+                        c.alloc(ids, nn)
+                    assert ei.value.code == err
+            assert c.num_free_blocks() == len(m.free)
+            for sid in range(16):
+                if sid in m.table:
+                    assert c.seq_info(sid) == (m.length[sid], m.table[sid])
+                else:
+                    with pytest.raises(A.ApexError) as ei:
+                        c.seq_info(sid)
+                    assert ei.value.code == "ESEQ"
+
+
+def test_alloc_errors_leave_state_unchanged():
+    c = host_cache(num_blocks=4)
+    c.alloc([0], [33])                      # 3 blocks
+    before = (c.num_free_blocks(), c.seq_info(0))
+    for ids, nn, code in [([1, 2], [16, 1], "ENOBLOCKS"), ([0, 0], [1, 1], "EINVAL"), ([99], [1], "EINVAL"),
+                          ([3], [0], "EINVAL"), ([3], [-1], "EINVAL"), ([3], [32 * 16 + 1], "EINVAL")]:
+        with pytest.raises(A.ApexError) as ei:
+            c.alloc(ids, nn)
+        assert ei.value.code == code
+        assert (c.num_free_blocks(), c.seq_info(0)) == before
+    c.release(0)
+    with pytest.raises(A.ApexError) as ei:
+        c.release(0)
+    assert ei.value.code == "ESEQ"
+    with pytest.raises(A.ApexError) as ei:
+        A.apex_kv_append(c.handle, 0, 0, 0)
+    assert ei.value.code == "EINVAL"
+
+
+def test_desc_validation():
+    for kw, code in [(dict(num_q_heads=6, num_kv_heads=4), "EINVAL"), (dict(head_dim=64), "EUNSUPPORTED"),
+                     (dict(block_size=32), "EUNSUPPORTED"), (dict(dtype="f32"), "EUNSUPPORTED"),
+                     (dict(num_q_heads=48, num_kv_heads=3), "EUNSUPPORTED"), (dict(max_batch=17), "EINVAL")]:
+        with pytest.raises(A.ApexError) as ei:
+            host_cache(**kw)
+        assert ei.value.code == code, kw
+    host_cache(dtype="f32", num_q_heads=4, num_kv_heads=4)      # fp32 MHA is supported
+    host_cache(dtype="f16", num_q_heads=32, num_kv_heads=32)
+
+
+def _check_plan(c, lens, hkv, bs=16):
+    items, n_merges = c.plan()
+    cover = {}
+    parts = {}
+    for (b, g, blk0, nblk, part, seq) in items:
+        assert nblk >= 1 and seq == c.batch_seq_ids[b]
+        for j in range(blk0, blk0 + nblk):
+            key = (b, g, j)
+            assert key not in cover
+            cover[key] = part
+        if part >= 0:
+            parts.setdefault((b, g), []).append((blk0, part))
+    want = {(b, g, j) for b, L in enumerate(lens) for g in range(hkv) for j in range(-(-L // bs))}
+    assert set(cover) == want
+    # split pairs: partial slots are consecutive in split (block) order and unique
+    all_slots = []
+    for key, lst in parts.items():
+        lst.sort()
+        slots = [p for _, p in lst]
+        assert slots == list(range(slots[0], slots[0] + len(slots))) and len(slots) >= 2
+        all_slots += slots
+    assert len(all_slots) == len(set(all_slots)) and n_merges == len(parts)
+    # longest-first order
+    assert all(items[i][3] >= items[i + 1][3] for i in range(len(items) - 1))
+    return items, n_merges
+
+
+def test_planner_coverage_random():
+    rnd = random.Random(1)
+    for trial in range(30):
+        hkv = rnd.choice([1, 2, 8])
+        c = host_cache(num_q_heads=hkv * rnd.choice([1, 4]) if hkv != 8 else 32, num_kv_heads=hkv,
+                       num_blocks=4096, max_blocks_per_seq=512, dtype="f16", max_new_tokens=1 << 16)
+        c.set_grid(rnd.choice([0, 1, 7, 296]))
+        if rnd.random() < 0.5:
+            c.set_split(16 * rnd.choice([1, 2, 5, 64]))
+        B = rnd.randint(1, 8)
+        lens = [rnd.randint(1, 2000) for _ in range(B)]
+        c.alloc(list(range(B)), lens)
+        _check_plan(c, lens, hkv)
+
+
+def test_planner_split_chunk_and_auto():
+    c = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=4096, max_blocks_per_seq=512)
+    c.set_split(64)                                  # 4 blocks per item
+    c.alloc([0, 1], [100, 64])                       # 7 blocks -> 4+3 ; 4 blocks -> unsplit
+    items, nm = _check_plan(c, [100, 64], 8)
+    assert nm == 8 and sum(1 for it in items if it[4] < 0) == 8
+    c2 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024, max_new_tokens=1 << 20)
+    c2.set_grid(296)
+    c2.alloc(list(range(4)), [16000] * 4)            # T = 4*1000*8 = 32000 blocks -> chunk 7 blocks
+    items, nm = _check_plan(c2, [16000] * 4, 8)
+    assert len(items) >= 16 * 296 * 0.9 and nm == 32
+    with pytest.raises(A.ApexError):
+        c2.set_split(10)                             # not a multiple of 16
+
+
+def test_cost_model_matches_oracle_interp():
+    rnd = random.Random(2)
+    for trial in range(50):
+        nb, nk = rnd.randint(1, 5), rnd.randint(1, 6)
+        bg = sorted(rnd.sample(range(1, 2048), nb))
+        kg = sorted(rnd.sample(range(1, 1 << 24), nk))
+        us = [[rnd.uniform(1, 5000) for _ in kg] for _ in bg]
+        h = A.apex_cost_create(bg, kg, us)
+        try:
+            for i, b in enumerate(bg):
+                for j, k in enumerate(kg):
+                    assert A.apex_predict_time(h, b, k) == us[i][j]
+            for _ in range(200):
+                b, k = rnd.randint(0, 4096), rnd.randint(0, 1 << 25)
+                assert A.apex_predict_time(h, b, k) == pytest.approx(cm.interp(bg, kg, us, b, k), rel=1e-12)
+        finally:
+            A.apex_cost_destroy(h)
+
+
+def test_cost_model_spec_example_and_validation():
+    h = A.apex_cost_create([1, 256], [4096], [[100.0], [110.0]])
+    assert A.apex_predict_time(h, 128, 4096) == pytest.approx(100 + 127 / 255 * 10, rel=1e-15)   # SPEC S:47 (fixed)
+    assert A.apex_predict_time(h, 1024, 4096) == 110.0 and A.apex_predict_time(h, 1, 1) == 100.0
+    A.apex_cost_destroy(h)
+    for bg, kg, us in [([2, 1], [1], [[1.0], [1.0]]), ([1], [5, 5], [[1.0, 1.0]]), ([1], [1], [[0.0]]),
+                       ([1], [1], [[float("nan")]]), ([0], [1], [[1.0]])]:
+        with pytest.raises(A.ApexError) as ei:
+            A.apex_cost_create(bg, kg, us)
+        assert ei.value.code == "EINVAL"
