@@ -89,7 +89,7 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     return w;
 }
 
-apex_status validate_desc(const apex_kv_desc *d) {
+apex_status validate_desc(const apex_kv_desc *d, bool need_workspace = true) {
     if (!d) return fail(APEX_EINVAL, "desc is NULL");
     if (d->num_layers < 1 || d->num_layers > apex::kMaxLayers)
         return fail(APEX_EINVAL, "num_layers %d not in [1, %d]", d->num_layers, apex::kMaxLayers);
@@ -114,14 +114,14 @@ apex_status validate_desc(const apex_kv_desc *d) {
         return fail(APEX_EUNSUPPORTED, "pool rows exceed the TMA coordinate range");
     if (d->max_batch > d->max_seqs) return fail(APEX_EINVAL, "max_batch > max_seqs");
     if (!desc_host_only(d)) {
-        if (!d->k_pool || !d->v_pool || !d->block_table || !d->seq_lens || !d->workspace)
+        if (!d->k_pool || !d->v_pool || !d->block_table || !d->seq_lens || (need_workspace && !d->workspace))
             return fail(APEX_EINVAL, "device desc needs k_pool, v_pool, block_table, seq_lens, workspace");
         for (int l = 0; l < d->num_layers; ++l) {
             if (!d->k_pool[l] || !d->v_pool[l]) return fail(APEX_EINVAL, "pool pointer of layer %d is NULL", l);
             if (((uintptr_t)d->k_pool[l] | (uintptr_t)d->v_pool[l]) & 127)
                 return fail(APEX_EINVAL, "pools of layer %d are not 128-byte aligned", l);
         }
-        if ((uintptr_t)d->workspace & 255) return fail(APEX_EINVAL, "workspace not 256-byte aligned");
+        if (need_workspace && ((uintptr_t)d->workspace & 255)) return fail(APEX_EINVAL, "workspace not 256-byte aligned");
     }
     return APEX_OK;
 }
@@ -219,7 +219,7 @@ const char *apex_last_error(void) { return g_err.c_str(); }
 const char *apex_version(void) { return "apex-b200 0.1 (sm_100a)"; }
 
 size_t apex_kv_workspace_bytes(const apex_kv_desc *desc) {
-    if (validate_desc(desc) != APEX_OK) return 0;
+    if (validate_desc(desc, false) != APEX_OK) return 0;
     return layout_for(desc, query_sm_count(desc_host_only(desc))).total;
 }
 

@@ -45,6 +45,8 @@ class PagedKVCache:
             return
         import torch
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         tdt = torch_dtype(dtype)
         shape = (num_blocks, num_kv_heads, block_size, head_dim)
         self.k_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
