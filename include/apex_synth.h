@@ -6,8 +6,10 @@
  * can be created on the GPU and any row regenerated on the host for the
  * oracle without reading device memory (SURVEY.md §8(d) "Synthetic inputs").
  *
- *   key = tensor<<55 | layer<<49 | b<<33 | head<<26 | t<<8 | d
- *   h   = splitmix64(key ^ splitmix64(seed));  x = ((h>>40) - 2^23) * 2^-22 * amp
+ *   rowkey = tensor<<55 | layer<<49 | b<<33 | head<<26 | t<<8
+ *   hrow   = splitmix64(rowkey ^ splitmix64(seed))
+ *   u      = lowbias32(lo32(hrow) + d * 0x9E3779B9) ^ hi32(hrow)
+ *   x      = ((u>>8) - 2^23) * 2^-22 * amp
  *   stored as fp32, or rounded to nearest even to fp16 / bf16.
  */
 #ifndef APEX_SYNTH_H

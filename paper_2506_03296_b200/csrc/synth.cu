@@ -16,6 +16,14 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return z ^ (z >> 31);
 }
 
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    return x ^ (x >> 16);
+}
+
 // key field shifts (must match synth/gen.py)
 constexpr int kT = 8, kH = 26, kB = 33, kL = 49, kX = 55;
 
@@ -33,11 +41,13 @@ __global__ void __launch_bounds__(256) apex_synth_kernel(void *out, int tensor, 
         const int64_t r = rh / n_heads;
         const uint64_t base = ((uint64_t)tensor << kX) | ((uint64_t)layer << kL) | ((uint64_t)row_b[r] << kB) |
                               ((uint64_t)(head_offset + h) << kH) | ((uint64_t)row_pos[r] << kT);
+        const uint64_t hrow = splitmix64(base ^ seedmix);
+        const uint32_t lo = (uint32_t)hrow, hi = (uint32_t)(hrow >> 32);
         float x[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const uint64_t hsh = splitmix64((base | (uint64_t)(d0 + e)) ^ seedmix);
-            const int32_t v = (int32_t)(hsh >> 40) - (1 << 23);
+            const uint32_t u = lowbias32(lo + (uint32_t)(d0 + e) * 0x9E3779B9u) ^ hi;
+            const int32_t v = (int32_t)(u >> 8) - (1 << 23);
             x[e] = ((float)v * 2.384185791015625e-07f) * amp;   // 2^-22, exact
         }
         const int64_t o = i * 8;

@@ -9,10 +9,15 @@ checks them bit-for-bit.
 
 Generator (SURVEY.md §8(d) "Synthetic inputs"):
 
-    key  = tensor<<55 | layer<<49 | b<<33 | head<<26 | t<<8 | d
-    h    = splitmix64(key XOR splitmix64(seed))
-    x    = ((h >> 40) - 2**23) * 2**-22          # exact in fp32, uniform [-2, 2)
-    x16  = round-to-nearest-even(x * amp)         # fp16 / bf16 bit patterns
+    rowkey = tensor<<55 | layer<<49 | b<<33 | head<<26 | t<<8      (the d field is 0)
+    hrow   = splitmix64(rowkey XOR splitmix64(seed))             # one per (row, head)
+    u      = lowbias32(lo32(hrow) + d * 0x9E3779B9) XOR hi32(hrow)  # uint32 arithmetic
+    x      = ((u >> 8) - 2**23) * 2**-22          # exact in fp32, uniform [-2, 2)
+    x16    = round-to-nearest-even(x * amp)       # fp16 / bf16 bit patterns
+
+lowbias32 is Wellons' 32-bit integer finaliser (x ^= x>>16; x *= 0x7feb352d;
+x ^= x>>15; x *= 0x846ca68b; x ^= x>>16).  One 64-bit mix per 128-dim row keeps
+the device fill of 100+ GiB caches cheap.
 
 ``amp`` is a power of two (q x1, x8, x64 variants), so ``x * amp`` is exact in
 fp32.  Values are keyed by logical (tensor, layer, request b, head, position t,
@@ -60,10 +65,23 @@ def make_key(tensor, layer, b, head, t, d) -> np.ndarray:
            (u(t) << np.uint64(_T_SHIFT)) | u(d)
 
 
+def lowbias32(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, dtype=np.uint32)
+    x = x ^ (x >> np.uint32(16))
+    x = x * np.uint32(0x7FEB352D)
+    x = x ^ (x >> np.uint32(15))
+    x = x * np.uint32(0x846CA68B)
+    return x ^ (x >> np.uint32(16))
+
+
 def gen_f32(tensor, layer, b, head, t, d, seed: int = 0, amp: float = 1.0) -> np.ndarray:
     """fp32 values for broadcastable index arrays (exact: 24-bit lattice times a power of two)."""
-    h = splitmix64(make_key(tensor, layer, b, head, t, d) ^ np.uint64(splitmix64_int(seed)))
-    v = (h >> np.uint64(40)).astype(np.int64) - (1 << 23)
+    hrow = splitmix64(make_key(tensor, layer, b, head, t, 0) ^ np.uint64(splitmix64_int(seed)))
+    lo = (hrow & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    hi = (hrow >> np.uint64(32)).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        u = lowbias32(lo + np.asarray(d, dtype=np.uint32) * np.uint32(0x9E3779B9)) ^ hi
+    v = (u >> np.uint32(8)).astype(np.int64) - (1 << 23)
     return (v.astype(np.float32) * np.float32(2.0 ** -22)) * np.float32(amp)
 
 
