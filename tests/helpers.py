@@ -30,11 +30,24 @@ def gen_dev(cache, tensor, layer, seqs, positions, heads, seed=0, amp=1.0):
     return synth_rows(out, cache.dtype, tensor, layer, rb, rp, seed=seed, amp=amp)
 
 
-def prefill(cache, seq_ids, ctx, layer=0, seed=0, chunk_seqs=None, interleave=0):
+def prefill(cache, seq_ids, ctx, layer=0, seed=0, interleave=0, max_rows=1 << 22, b_ids=None):
     """Write positions 0..ctx[i]-2 of each seq (the decode step appends ctx[i]-1).
 
     interleave > 0 grows the sequences `interleave` tokens at a time round-robin,
-    scattering their physical blocks."""
+    scattering their physical blocks.  Sequences are prefilled in groups of at
+    most max_rows rows.  b_ids maps seq ids to generator request ids (default: same)."""
+    if interleave == 0:
+        group, rows = [], 0
+        for s, c in zip(seq_ids, ctx):
+            if group and rows + c - 1 > max_rows:
+                prefill(cache, [g for g, _ in group], [c2 for _, c2 in group], layer, seed, -1, max_rows, b_ids)
+                group, rows = [], 0
+            group.append((s, c))
+            rows += c - 1
+        if group:
+            prefill(cache, [g for g, _ in group], [c2 for _, c2 in group], layer, seed, -1, max_rows, b_ids)
+        return
+    bid = (lambda s: s) if b_ids is None else (lambda s: b_ids[s])
     todo = {s: c - 1 for s, c in zip(seq_ids, ctx) if c > 1}
     have = {s: 0 for s in todo}
     while todo:
@@ -46,7 +59,7 @@ def prefill(cache, seq_ids, ctx, layer=0, seed=0, chunk_seqs=None, interleave=0)
         cache.alloc(ids, nn)
         rows_b, rows_p = [], []
         for s, n in zip(ids, nn):
-            rows_b += [s] * n
+            rows_b += [bid(s)] * n
             rows_p += list(range(have[s], have[s] + n))
             have[s] += n
             todo[s] -= n

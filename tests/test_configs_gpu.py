@@ -1,0 +1,67 @@
+"""Full-size parity for BASELINE.json configs C1-C5 (one physical layer each), in the
+launch configuration bench.py times (automatic split planner, persistent grid).
+
+C1 is checked on every row (fp32, q x1 and q x8); C2-C5 on >= 256 sampled rows
+(8 whole requests x all q heads, including the shortest and longest contexts of
+the ragged C4) against the float64 oracle on regenerated inputs (readings c6-c8).
+"""
+import numpy as np
+import pytest
+
+from helpers import check_close, decode_step, make_cache, oracle_rows, prefill, to_f64
+from synth import WORKLOADS
+
+pytestmark = pytest.mark.gpu
+
+
+def build(name, steps=1):
+    w = WORKLOADS[name]
+    ctx = [int(c) for c in w.contexts()]
+    B = len(ctx)
+    nb = sum(-(-(c + steps) // 16) for c in ctx) + 16
+    cache = make_cache(w.dtype, w.num_q_heads, w.num_kv_heads, nb, max_seqs=B,
+                       max_blocks_per_seq=-(-(max(ctx) + steps) // 16) + 1, max_new_tokens=1 << 22)
+    seqs = list(range(B))
+    prefill(cache, seqs, ctx)
+    return w, cache, seqs, ctx
+
+
+def sample_rows(ctx, hq, n_req=8):
+    order = np.argsort(ctx, kind="stable")
+    pick = sorted({int(order[0]), int(order[-1])} | {int(i) for i in np.linspace(0, len(ctx) - 1, n_req)})[:n_req]
+    return [b * hq + h for b in pick for h in range(hq)]
+
+
+@pytest.mark.parametrize("qamp", [1.0, 8.0])
+def test_c1_full(cuda_lib, qamp):
+    w, cache, seqs, ctx = build("c1")
+    out = to_f64(decode_step(cache, seqs, ctx, qamp=qamp), w.dtype)
+    ref = oracle_rows(seqs, ctx, w.num_q_heads, w.num_kv_heads, w.dtype, qamp=qamp)
+    check_close(out, ref, "f32")
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_uniform_configs_sampled(cuda_lib, name):
+    import torch
+    w, cache, seqs, ctx = build(name)
+    out = to_f64(decode_step(cache, seqs, ctx), w.dtype)
+    rows = sample_rows(ctx, w.num_q_heads)
+    assert len(rows) >= 256
+    ref = oracle_rows(seqs, ctx, w.num_q_heads, w.num_kv_heads, w.dtype, rows=rows)
+    check_close(out.reshape(-1, 128)[rows], ref, w.dtype)
+    del cache
+    torch.cuda.empty_cache()
+
+
+def test_c4_ragged_multistep_append(cuda_lib):
+    """C4: ragged 1K-32K contexts; 3 decode steps of alloc(+1) / append / attend."""
+    import torch
+    w, cache, seqs, ctx = build("c4", steps=3)
+    for s in range(3):
+        cur = [c + s for c in ctx]
+        out = to_f64(decode_step(cache, seqs, cur), w.dtype)
+    rows = sample_rows(cur, w.num_q_heads)
+    ref = oracle_rows(seqs, cur, w.num_q_heads, w.num_kv_heads, w.dtype, rows=rows)
+    check_close(out.reshape(-1, 128)[rows], ref, w.dtype)
+    del cache
+    torch.cuda.empty_cache()
