@@ -49,6 +49,6 @@ def gather_heads(out_local, group=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     B, hl, D = out_local.shape
-    full = torch.empty((world, B, hl, D), dtype=out_local.dtype, device=out_local.device)
+    full = torch.empty((world * B, hl, D), dtype=out_local.dtype, device=out_local.device)
     dist.all_gather_into_tensor(full, out_local.contiguous(), group=group)
-    return full.permute(1, 0, 2, 3).reshape(B, world * hl, D)
+    return full.view(world, B, hl, D).permute(1, 0, 2, 3).reshape(B, world * hl, D)
