@@ -416,11 +416,11 @@ def run_apex(args):
               "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,
               "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                            "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.config),
-                           "kernel": "apex_decode_attention (apex_decode_kernel + apex_merge_kernel)",
+                           "kernel": "apex_decode_attention (apex_decode_kernel, fused split-KV + LSE merge)",
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
-              "gpu_launches": K * (1 + L * (2 + (1 if n_merges else 0))),
+              "gpu_launches": K * (1 + 2 * L),     # apply-deltas + L x (append, decode)
               "prefill_s": t_fill}
     if clk:
         result["clocks"] = clk

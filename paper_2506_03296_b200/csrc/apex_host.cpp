@@ -63,15 +63,15 @@ int query_sm_count(bool host_only) {
 // merges, slots, block-table deltas, length deltas) into `upload`.
 struct WsLayout {
     int32_t max_items = 0, max_merges = 0, max_bt_delta = 0;
-    size_t counters = 0, upload = 0, upload_cap = 0, part_o = 0, part_ml = 0, total = 0;
+    size_t counters = 0, merge_counters = 0, upload = 0, upload_cap = 0, part_o = 0, part_ml = 0, total = 0;
 };
 
 WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     WsLayout w;
     const int G = d->num_q_heads / d->num_kv_heads;
     const int64_t pairs = (int64_t)d->max_batch * d->num_kv_heads;
-    // auto planner: items <= pairs + 16 * grid; grid <= 4 * SMs
-    w.max_items = (int32_t)std::min<int64_t>(pairs + 16LL * 4 * sm_count + 64, 1 << 24);
+    // auto planner: items <= pairs + 64 * grid (small pieces) ; grid <= 4 * SMs
+    w.max_items = (int32_t)std::min<int64_t>(pairs + 64LL * 4 * sm_count + 64, 1 << 24);
     w.max_merges = (int32_t)pairs;
     w.max_bt_delta = (int32_t)(cdiv(d->max_new_tokens, d->block_size) + d->max_batch);
     size_t up = 0;
@@ -80,8 +80,9 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     up += align_up(sizeof(int32_t) * (size_t)d->max_new_tokens, 256);
     up += align_up(sizeof(int2) * (size_t)w.max_bt_delta, 256);
     up += align_up(sizeof(int2) * (size_t)d->max_batch, 256);
-    w.counters = 0;
-    w.upload = 512;                                           // 2 counters x 64 layers
+    w.counters = 0;                                           // 2 counters x 64 layers
+    w.merge_counters = 512;                                   // one per split pair
+    w.upload = align_up(w.merge_counters + sizeof(int32_t) * (size_t)w.max_merges, 256);
     w.upload_cap = up;
     w.part_o = align_up(w.upload + up, 256);
     w.part_ml = align_up(w.part_o + sizeof(float) * (size_t)w.max_items * G * d->head_dim, 256);
@@ -282,8 +283,8 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
             apex_kv_destroy(kv);
             return cuda_fail(e, "apex_kv_create: decode kernel attributes");
         }
-        // zero the work-queue counters once; kernels leave them at zero
-        e = cudaMemset((uint8_t *)desc->workspace + kv->ws.counters, 0, 512);
+        // zero the work-queue and merge counters once; kernels leave them at zero
+        e = cudaMemset((uint8_t *)desc->workspace + kv->ws.counters, 0, kv->ws.upload);
         if (e != cudaSuccess) {
             apex_kv_destroy(kv);
             return cuda_fail(e, "apex_kv_create: counters");
@@ -353,37 +354,63 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
     return APEX_OK;
 }
 
-// Split-KV planner (FlashDecoding lineage): cut each (batch row, kv head)
-// pair into near-equal pieces of whole blocks so the persistent grid sees ~16
-// items per CTA, then order items longest-first (stable) for the dynamic queue.
+// Split-KV planner (FlashDecoding lineage).  T = total (block, kv-head)
+// tiles, P = persistent CTAs.
+//  * latency regime (T <= 64 P): uniform pieces of ceil(T/P) blocks, so every
+//    CTA gets about one item;
+//  * bandwidth regime: each (row, kv-head) pair is cut into whole "big" pieces
+//    of ceil(T/8P) blocks, and its remainder -- at least a reserve sized so that
+//    the whole plan has >= 2P small pieces -- into near-equal "small" pieces of
+//    <= ceil(T/64P) blocks.  Items run longest-first from the device queue, so
+//    the big pieces stream first and the small ones fill the tail: the finish
+//    spread is bounded by one small piece (~1/64 of a CTA's share).
+//  * a forced chunk (apex_kv_set_split) gives uniform pieces of that size.
+// A pair cut into >1 pieces gets partial slots and a merge entry.
 static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     const int32_t Hkv = kv->d.num_kv_heads, B = (int32_t)lens.size();
-    const int32_t P = kv->grid_override > 0 ? kv->grid_override
-                                            : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count);
+    const int64_t P = std::max<int64_t>(1, kv->grid_override > 0
+                                               ? kv->grid_override
+                                               : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
     int64_t T = 0;
     for (int32_t L : lens) T += cdiv(L, kv->d.block_size) * Hkv;
-    int64_t chunk = kv->forced_chunk_blocks > 0 ? kv->forced_chunk_blocks
-                                                : std::max<int64_t>(4, cdiv(T, 16LL * std::max(P, 1)));
+    int64_t big, small;
+    if (kv->forced_chunk_blocks > 0) {
+        big = small = kv->forced_chunk_blocks;
+    } else if (T <= 64 * P) {
+        big = small = std::max<int64_t>(1, cdiv(T, P));
+    } else {
+        big = std::max<int64_t>(16, cdiv(T, 8 * P));
+        small = std::max<int64_t>(4, cdiv(T, 64 * P));
+    }
+    const int64_t pairs = std::max<int64_t>(1, (int64_t)B * Hkv);
+    const int64_t reserve = big == small ? 0 : cdiv(2 * P * small, pairs);
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;
+    std::vector<int32_t> pieces;
     int32_t parts = 0;
     for (int32_t b = 0; b < B; ++b) {
         const int32_t nblk = (int32_t)cdiv(lens[b], kv->d.block_size);
-        const int32_t nsplit = (int32_t)cdiv(nblk, chunk);
+        pieces.clear();
+        const int32_t nbig = big == small ? 0 : (int32_t)(std::max<int64_t>(0, nblk - reserve) / big);
+        for (int32_t i = 0; i < nbig; ++i) pieces.push_back((int32_t)big);
+        const int32_t rem = nblk - nbig * (int32_t)big;
+        const int32_t nsm = (int32_t)cdiv(rem, small);
+        for (int32_t i = 0; i < nsm; ++i) pieces.push_back(rem / nsm + (i < rem % nsm ? 1 : 0));
+        const bool split = pieces.size() > 1;
         for (int32_t g = 0; g < Hkv; ++g) {
-            if (nsplit > 1) merges.push_back({b, g, parts, nsplit});
+            const int32_t mg = split ? (int32_t)merges.size() : -1;
+            if (split) merges.push_back({b, g, parts, (int32_t)pieces.size()});
             int32_t blk = 0;
-            for (int32_t i = 0; i < nsplit; ++i) {
-                const int32_t n = nblk / nsplit + (i < nblk % nsplit ? 1 : 0);
-                items.push_back({b, g, blk, n, nsplit > 1 ? parts + i : -1, kv->batch_seq[b], lens[b], 0});
-                blk += n;
+            for (size_t i = 0; i < pieces.size(); ++i) {
+                items.push_back({b, g, blk, pieces[i], split ? parts + (int32_t)i : -1, kv->batch_seq[b], lens[b], mg});
+                blk += pieces[i];
             }
-            if (nsplit > 1) parts += nsplit;
+            if (split) parts += (int32_t)pieces.size();
         }
     }
     if ((int64_t)items.size() > kv->ws.max_items)
-        return fail(APEX_EINVAL, "split chunk %lld tokens yields %zu work items > workspace capacity %d",
-                    (long long)chunk * kv->d.block_size, items.size(), kv->ws.max_items);
+        return fail(APEX_EINVAL, "split chunk of %lld tokens yields %zu work items > workspace capacity %d",
+                    (long long)small * kv->d.block_size, items.size(), kv->ws.max_items);
     std::stable_sort(items.begin(), items.end(),
                      [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
     kv->items.swap(items);
@@ -532,6 +559,7 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
     p.part_o = (float *)(ws + kv->ws.part_o);
     p.part_ml = (float *)(ws + kv->ws.part_ml);
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
+    p.merge_counters = (int32_t *)(ws + kv->ws.merge_counters);
     p.n_items = (int32_t)kv->items.size();
     p.n_merges = (int32_t)kv->merges.size();
     p.max_blocks_per_seq = kv->d.max_blocks_per_seq;

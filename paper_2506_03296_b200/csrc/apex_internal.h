@@ -24,10 +24,11 @@ struct __align__(16) WorkItem {
     int32_t part;     // partial slot, or -1 if the item covers the whole (b, g) pair
     int32_t seq;      // sequence id (block_table row)
     int32_t len;      // tokens of the sequence (masking of the last block)
-    int32_t pad;
+    int32_t mg;       // index into the merge list (split items), or -1
 };
 
 // One (b, g) pair whose items were split: partial slots [part0, part0+nparts).
+// The last item of the pair to finish merges the partials inside the decode kernel.
 struct __align__(16) MergeItem {
     int32_t b, g, part0, nparts;
 };
@@ -41,6 +42,7 @@ struct DecodeParams {
     float *part_o;             // [slots][G][D]   unnormalised sum_t p_t v_t (fp32)
     float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)
     int32_t *counters;         // [2]: work-queue head, CTAs done
+    int32_t *merge_counters;   // [n_merges]: split items finished per pair (left at 0)
     int32_t n_items;
     int32_t n_merges;
     int32_t max_blocks_per_seq;

@@ -22,8 +22,9 @@
 //  * MHA (g == 1) and fp32: CUDA-core FMAs, one lane per token for q.K
 //    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
-//    (m, l, unnormalised O) fp32 partials that merge_kernel combines in split
-//    order.
+//    (m, l, unnormalised O) fp32 partials; the last split of a (b, g) pair to
+//    finish (per-pair arrival counter) merges them in split order (fused LSE
+//    merge, no second launch).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -50,7 +51,7 @@ template <int DT, int G> struct Cfg {
     static constexpr int ES = DT == APEX_F32 ? 4 : 2;
     static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of one K (or V) tile
     static constexpr int CB_O = NC * G * kHeadDim * 4;       // per-warp O for the item merge
-    static constexpr int CB_ML = NC * G * 2 * 4;
+    static constexpr int CB_ML = NC * G * 2 * 4 + 16;     // + merge flag
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
     static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
@@ -411,6 +412,33 @@ template <int DT> struct SimtConsumer {
 template <int DT, int G> struct ConsumerSel { using T = MmaConsumer<DT, G>; };
 template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
 
+// log-sum-exp merge of one split (b, g) pair, partials combined in split order:
+// M = max m_i, out = sum 2^(m_i-M) O_i / sum 2^(m_i-M) l_i.  Partials written by
+// other CTAs are read through L2 (ld.global.cg).
+template <int DT, int G>
+__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt) {
+    for (int idx = t; idx < G * kHeadDim / 4; idx += nt) {
+        const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+        float M = -INFINITY;
+        for (int i = 0; i < mg.nparts; ++i)
+            M = fmaxf(M, __ldcg(p.part_ml + ((size_t)(mg.part0 + i) * G + row) * 2));
+        float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+        for (int i = 0; i < mg.nparts; ++i) {
+            const size_t pi = (size_t)(mg.part0 + i) * G + row;
+            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(p.part_ml + pi * 2));
+            const float e = ex2_diff(ml.x, M);
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4));
+            den = fmaf(e, ml.y, den);
+            a = fmaf(e, v.x, a);
+            b = fmaf(e, v.y, b);
+            c = fmaf(e, v.z, c);
+            d = fmaf(e, v.w, d);
+        }
+        const size_t o = ((size_t)mg.b * p.num_q_heads + (size_t)mg.g * G + row) * kHeadDim + d4;
+        store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
+    }
+}
+
 // ------------------------------------------------------------------ decode kernel
 template <int DT, int G>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
@@ -426,6 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     float *cb_o = reinterpret_cast<float *>(smem + S::TILES + S::BARS + S::RING);
     float *cb_m = cb_o + NC * G * kHeadDim;
     float *cb_l = cb_m + NC * G;
+    volatile int *merge_flag = reinterpret_cast<volatile int *>(cb_l + NC * G);
     const uint32_t tiles_u = smem_u32(smem);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES;
     const uint32_t ifull0 = empty0 + 8 * STAGES, iempty0 = ifull0 + 8 * IR;
@@ -556,33 +585,24 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (d4 == 0) *reinterpret_cast<float2 *>(p.part_ml + ((size_t)it.part * G + row) * 2) = make_float2(M, den);
                 }
             }
+            if (it.part >= 0) {
+                // last-arriving split of this (b, g) pair merges all its partials (fused LSE merge)
+                __threadfence();
+                named_bar_sync(1, NC * 32);
+                if (threadIdx.x == 32) {
+                    const int done = atomicAdd(p.merge_counters + it.mg, 1);
+                    const int last = done == p.merges[it.mg].nparts - 1;
+                    if (last) p.merge_counters[it.mg] = 0;      // every split has arrived: re-arm
+                    *merge_flag = last;
+                }
+                named_bar_sync(1, NC * 32);
+                if (*merge_flag) {
+                    __threadfence();
+                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32);
+                }
+            }
             named_bar_sync(1, NC * 32);
         }
-    }
-}
-
-// log-sum-exp merge of split items (fixed split order): one CTA per (b, g) pair
-template <int DT, int G>
-__global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
-    const MergeItem mg = p.merges[blockIdx.x];
-    for (int idx = threadIdx.x; idx < G * kHeadDim / 4; idx += blockDim.x) {
-        const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
-        float M = -INFINITY;
-        for (int i = 0; i < mg.nparts; ++i) M = fmaxf(M, p.part_ml[((size_t)(mg.part0 + i) * G + row) * 2]);
-        float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
-        for (int i = 0; i < mg.nparts; ++i) {
-            const size_t pi = (size_t)(mg.part0 + i) * G + row;
-            const float2 ml = *reinterpret_cast<const float2 *>(p.part_ml + pi * 2);
-            const float e = ex2_diff(ml.x, M);
-            const float4 v = *reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4);
-            den = fmaf(e, ml.y, den);
-            a = fmaf(e, v.x, a);
-            b = fmaf(e, v.y, b);
-            c = fmaf(e, v.z, c);
-            d = fmaf(e, v.w, d);
-        }
-        const size_t o = ((size_t)mg.b * p.num_q_heads + (size_t)mg.g * G + row) * kHeadDim + d4;
-        store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
     }
 }
 
@@ -593,16 +613,9 @@ template <int DT, int G> cudaError_t prepare() {
 
 template <int DT, int G>
 cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
-    if (grid > 0) {
-        apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    if (p.n_merges > 0) {
-        apex_merge_kernel<DT, G><<<p.n_merges, 128, 0, s>>>(p);
-        return cudaGetLastError();
-    }
-    return cudaSuccess;
+    if (grid <= 0) return cudaSuccess;
+    apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
+    return cudaGetLastError();
 }
 
 }  // namespace

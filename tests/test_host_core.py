@@ -164,9 +164,16 @@ def test_planner_split_chunk_and_auto():
     assert nm == 8 and sum(1 for it in items if it[4] < 0) == 8
     c2 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024, max_new_tokens=1 << 20)
     c2.set_grid(296)
-    c2.alloc(list(range(4)), [16000] * 4)            # T = 4*1000*8 = 32000 blocks -> chunk 7 blocks
+    c2.alloc(list(range(4)), [16000] * 4)            # T = 32000 tiles > 64P: big 16 blocks, small 4
     items, nm = _check_plan(c2, [16000] * 4, 8)
-    assert len(items) >= 16 * 296 * 0.9 and nm == 32
+    # reserve ceil(2*296*4/32) = 74 blocks per pair for small pieces: 57 big (16) + 22 small (4)
+    assert len(items) == 32 * (57 + 22) and nm == 32
+    assert max(it[3] for it in items[-2 * 296:]) <= 4     # the queue tail holds only small pieces
+    c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024)
+    c3.set_grid(296)
+    c3.alloc([0], [1000])                            # T = 63*8 = 504 <= 64P: ~1 item per CTA
+    items, nm = _check_plan(c3, [1000], 8)
+    assert len(items) == 8 * 32 and all(it[3] == 2 for it in items[:-8])
     with pytest.raises(A.ApexError):
         c2.set_split(10)                             # not a multiple of 16
 
