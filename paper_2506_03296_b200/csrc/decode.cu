@@ -479,11 +479,24 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
+        // The control path (queue atomic -> item -> block-table entries) is
+        // software-pipelined one item ahead, and block-table entries one
+        // 32-entry chunk ahead, so the TMA stream never waits on a dependent
+        // global load at item or chunk boundaries.
         int32_t issued = 0;
+        auto bt_row = [&](const WorkItem &w) {
+            return p.block_table + (size_t)w.seq * p.max_blocks_per_seq + w.blk0;
+        };
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(p.counters, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        WorkItem it{};
+        int my = 0;
+        if (idx < p.n_items) {
+            it = p.items[idx];
+            my = lane < it.nblk ? __ldg(bt_row(it) + lane) : 0;
+        }
         for (int k = 0;; ++k) {
-            int idx = 0;
-            if (lane == 0) idx = atomicAdd(p.counters, 1);
-            idx = __shfl_sync(0xffffffffu, idx, 0);
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
@@ -494,17 +507,34 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
-            const WorkItem it = p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
-            const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
+            int nidx = 0;                                     // next item: claimed now, used later
+            if (lane == 0) nidx = atomicAdd(p.counters, 1);
+            WorkItem nit{};
+            int nmy = 0;
+            bool got_idx = false, got_item = false, got_bt = false;
+            auto advance_next = [&](int t) {                  // staged so each load has time to land
+                if (!got_idx && t >= 1) {
+                    nidx = __shfl_sync(0xffffffffu, nidx, 0);
+                    if (nidx < p.n_items) nit = p.items[nidx];
+                    got_idx = true;
+                }
+                if (got_idx && !got_item && t >= 3) {
+                    got_item = true;
+                    if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
+                    got_bt = true;
+                }
+            };
+            const int32_t *bt = bt_row(it);
+            int t = 0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
+                const int my_next = (j0 + 32 + lane < it.nblk) ? __ldg(bt + j0 + 32 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
-                for (int jj = 0; jj < cnt; ++jj) {
+                for (int jj = 0; jj < cnt; ++jj, ++t) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
                     if (lane == 0) {
                         const int s = issued % STAGES, u = issued / STAGES;
@@ -523,9 +553,17 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                             }
                         }
                     }
+                    __syncwarp();
                     ++issued;
+                    advance_next(t);
                 }
+                my = my_next;
             }
+            advance_next(1 << 30);
+            (void)got_bt;
+            idx = nidx;
+            it = nit;
+            my = nmy;
         }
         // last CTA out resets the queue for the next launch on this layer
         if (lane == 0) {
