@@ -12,7 +12,7 @@ import ctypes
 import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libapex.so")
+LIB_PATH = os.environ.get("APEX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libapex.so")
 
 APEX_OK, APEX_EINVAL, APEX_ENOBLOCKS, APEX_ESEQ, APEX_ECUDA, APEX_EUNSUPPORTED = range(6)
 STATUS_NAMES = {0: "APEX_OK", 1: "APEX_EINVAL", 2: "APEX_ENOBLOCKS", 3: "APEX_ESEQ", 4: "APEX_ECUDA",
