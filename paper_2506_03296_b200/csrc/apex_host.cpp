@@ -212,6 +212,7 @@ struct apex_kv {
 
     std::vector<apex::TmaPair> tmaps;
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
+    bool fuse_merge = false;
 };
 
 extern "C" {
@@ -415,6 +416,7 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
                      [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
     kv->items.swap(items);
     kv->merges.swap(merges);
+    kv->fuse_merge = big == small && kv->forced_chunk_blocks == 0;   // latency regime: save the launch
     return APEX_OK;
 }
 
@@ -567,6 +569,7 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
     p.num_kv_heads = kv->d.num_kv_heads;
     p.scale_log2 = (float)((double)scale * 1.4426950408889634);   // log2(e)
     p.tma_segs = kv->tma_segs;
+    p.fuse_merge = kv->fuse_merge ? 1 : 0;
     const int grid = std::min<int>(p.n_items, apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
     cudaError_t e = apex::launch_decode(kv->d.dtype, kv->group, kv->tmaps[layer], p, grid, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_decode_attention");

@@ -50,6 +50,7 @@ struct DecodeParams {
     int32_t num_kv_heads;
     float scale_log2;          // scale * log2(e)
     int32_t tma_segs;          // 1: one 3-D TMA op per tile; n: n 2-D ops (one per 128-B segment)
+    int32_t fuse_merge;        // 1: last split per pair merges in-kernel; 0: apex_merge_kernel launch
 };
 
 struct TmaPair {

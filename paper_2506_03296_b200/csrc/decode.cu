@@ -22,9 +22,10 @@
 //  * MHA (g == 1) and fp32: CUDA-core FMAs, one lane per token for q.K
 //    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
-//    (m, l, unnormalised O) fp32 partials; the last split of a (b, g) pair to
-//    finish (per-pair arrival counter) merges them in split order (fused LSE
-//    merge, no second launch).
+//    (m, l, unnormalised O) fp32 partials merged in split order -- by a second
+//    small launch (one CTA per split pair) in the bandwidth regime, or, in the
+//    latency regime, by the last split of the pair to finish (per-pair arrival
+//    counter) inside this kernel, saving the launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -479,24 +480,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
-        // The control path (queue atomic -> item -> block-table entries) is
-        // software-pipelined one item ahead, and block-table entries one
-        // 32-entry chunk ahead, so the TMA stream never waits on a dependent
-        // global load at item or chunk boundaries.
         int32_t issued = 0;
-        auto bt_row = [&](const WorkItem &w) {
-            return p.block_table + (size_t)w.seq * p.max_blocks_per_seq + w.blk0;
-        };
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(p.counters, 1);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        WorkItem it{};
-        int my = 0;
-        if (idx < p.n_items) {
-            it = p.items[idx];
-            my = lane < it.nblk ? __ldg(bt_row(it) + lane) : 0;
-        }
         for (int k = 0;; ++k) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.counters, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
@@ -507,34 +495,17 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
+            const WorkItem it = p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
-            int nidx = 0;                                     // next item: claimed now, used later
-            if (lane == 0) nidx = atomicAdd(p.counters, 1);
-            WorkItem nit{};
-            int nmy = 0;
-            bool got_idx = false, got_item = false, got_bt = false;
-            auto advance_next = [&](int t) {                  // staged so each load has time to land
-                if (!got_idx && t >= 1) {
-                    nidx = __shfl_sync(0xffffffffu, nidx, 0);
-                    if (nidx < p.n_items) nit = p.items[nidx];
-                    got_idx = true;
-                }
-                if (got_idx && !got_item && t >= 3) {
-                    got_item = true;
-                    if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
-                    got_bt = true;
-                }
-            };
-            const int32_t *bt = bt_row(it);
-            int t = 0;
+            const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my_next = (j0 + 32 + lane < it.nblk) ? __ldg(bt + j0 + 32 + lane) : 0;
+                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
-                for (int jj = 0; jj < cnt; ++jj, ++t) {
+                for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
                     if (lane == 0) {
                         const int s = issued % STAGES, u = issued / STAGES;
@@ -553,17 +524,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                             }
                         }
                     }
-                    __syncwarp();
                     ++issued;
-                    advance_next(t);
                 }
-                my = my_next;
             }
-            advance_next(1 << 30);
-            (void)got_bt;
-            idx = nidx;
-            it = nit;
-            my = nmy;
         }
         // last CTA out resets the queue for the next launch on this layer
         if (lane == 0) {
@@ -623,7 +586,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (d4 == 0) *reinterpret_cast<float2 *>(p.part_ml + ((size_t)it.part * G + row) * 2) = make_float2(M, den);
                 }
             }
-            if (it.part >= 0) {
+            if (it.part >= 0 && p.fuse_merge) {
                 // last-arriving split of this (b, g) pair merges all its partials (fused LSE merge)
                 __threadfence();
                 named_bar_sync(1, NC * 32);
@@ -644,6 +607,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     }
 }
 
+// log-sum-exp merge of split pairs as its own launch (bandwidth regime): one CTA
+// per (b, g) pair, so merging never stalls a decode CTA's TMA stream.
+template <int DT, int G>
+__global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
+    merge_pair<DT, G>(p, p.merges[blockIdx.x], threadIdx.x, blockDim.x);
+}
+
 template <int DT, int G> cudaError_t prepare() {
     return cudaFuncSetAttribute(apex_decode_kernel<DT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Cfg<DT, G>::TOTAL);
@@ -651,9 +621,16 @@ template <int DT, int G> cudaError_t prepare() {
 
 template <int DT, int G>
 cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
-    if (grid <= 0) return cudaSuccess;
-    apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
-    return cudaGetLastError();
+    if (grid > 0) {
+        apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || p.fuse_merge || p.n_merges == 0) return e;
+    }
+    if (p.n_merges > 0) {
+        apex_merge_kernel<DT, G><<<p.n_merges, 128, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
 }
 
 }  // namespace
