@@ -8,6 +8,8 @@
 // profiler + performance model.  Allocation contract:
 // DESIGN.md reading c10.
 #include <algorithm>
+#include <cstdlib>
+#include <functional>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -213,6 +215,12 @@ struct apex_kv {
     std::vector<apex::TmaPair> tmaps;
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
     bool fuse_merge = false;
+    int64_t last_chunk = 0;
+    struct {
+        bool valid;
+        int32_t B;
+        int64_t P, T, chunk;
+    } plan_cache{false, 0, 0, 0, 0};
 };
 
 extern "C" {
@@ -310,12 +318,14 @@ apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens) {
         return fail(APEX_EINVAL, "chunk_tokens %d must be a non-negative multiple of %d", chunk_tokens,
                     kv->d.block_size);
     kv->forced_chunk_blocks = chunk_tokens / kv->d.block_size;
+    kv->plan_cache.valid = false;
     return APEX_OK;
 }
 
 apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas) {
     if (!kv || ctas < 0) return fail(APEX_EINVAL, "bad grid override");
     kv->grid_override = ctas;
+    kv->plan_cache.valid = false;
     return APEX_OK;
 }
 
@@ -356,67 +366,112 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
 }
 
 // Split-KV planner (FlashDecoding lineage).  T = total (block, kv-head)
-// tiles, P = persistent CTAs.
-//  * latency regime (T <= 64 P): uniform pieces of ceil(T/P) blocks, so every
-//    CTA gets about one item;
-//  * bandwidth regime: each (row, kv-head) pair is cut into whole "big" pieces
-//    of ceil(T/8P) blocks, and its remainder -- at least a reserve sized so that
-//    the whole plan has >= 2P small pieces -- into near-equal "small" pieces of
-//    <= ceil(T/64P) blocks.  Items run longest-first from the device queue, so
-//    the big pieces stream first and the small ones fill the tail: the finish
-//    spread is bounded by one small piece (~1/64 of a CTA's share).
-//  * a forced chunk (apex_kv_set_split) gives uniform pieces of that size.
+// tiles, P = persistent CTAs.  Each (row, kv-head) pair is cut into
+// near-equal pieces of at most `chunk` blocks; items run longest-first from
+// the device queue (greedy LPT on P CTAs).
+//  * latency regime (T <= 64 P): chunk = ceil(T/P), about one item per CTA, and
+//    the LSE merge is fused into the decode kernel (saves a launch);
+//  * bandwidth regime: candidate chunks (no split, T/(kP) for k in 4..32) are
+//    scored by simulating the LPT schedule -- makespan in tiles + a per-item
+//    cost (~1 tile: item fetch/merge bookkeeping) + a fixed cost if a merge
+//    launch is needed -- and the cheapest wins.  The choice is cached and only
+//    re-evaluated when the batch or T changes by > 2% (the simulation is
+//    O(items log P) host work);
+//  * a forced chunk (apex_kv_set_split) is used as is.
 // A pair cut into >1 pieces gets partial slots and a merge entry.
+namespace {
+void pieces_of(int32_t nblk, int64_t chunk, std::vector<int32_t> &out) {
+    out.clear();
+    const int32_t n = (int32_t)cdiv(nblk, chunk);
+    for (int32_t i = 0; i < n; ++i) out.push_back(nblk / n + (i < nblk % n ? 1 : 0));
+}
+
+// LPT makespan (tiles) of the item multiset produced by `chunk` + overheads
+double plan_cost(const std::vector<int32_t> &nblks, int32_t hkv, int64_t chunk, int64_t P) {
+    std::vector<int32_t> sizes, pc;
+    int64_t merges = 0;
+    for (int32_t nb : nblks) {
+        pieces_of(nb, chunk, pc);
+        if (pc.size() > 1) merges += hkv;
+        for (int32_t g = 0; g < hkv; ++g) sizes.insert(sizes.end(), pc.begin(), pc.end());
+    }
+    std::sort(sizes.begin(), sizes.end(), std::greater<int32_t>());
+    std::vector<int64_t> heap((size_t)P, 0);   // min-heap of CTA loads
+    for (int32_t sz : sizes) {
+        std::pop_heap(heap.begin(), heap.end(), std::greater<int64_t>());
+        heap.back() += sz + 1;                  // + ~1 tile of per-item cost
+        std::push_heap(heap.begin(), heap.end(), std::greater<int64_t>());
+    }
+    const int64_t makespan = *std::max_element(heap.begin(), heap.end());
+    return (double)makespan + (merges ? 12.0 + 2.0 * (double)merges / (double)P : 0.0);
+}
+}  // namespace
+
 static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     const int32_t Hkv = kv->d.num_kv_heads, B = (int32_t)lens.size();
     const int64_t P = std::max<int64_t>(1, kv->grid_override > 0
                                                ? kv->grid_override
                                                : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
+    std::vector<int32_t> nblks(B);
     int64_t T = 0;
-    for (int32_t L : lens) T += cdiv(L, kv->d.block_size) * Hkv;
-    int64_t big, small;
-    if (kv->forced_chunk_blocks > 0) {
-        big = small = kv->forced_chunk_blocks;
-    } else if (T <= 64 * P) {
-        big = small = std::max<int64_t>(1, cdiv(T, P));
-    } else {
-        big = std::max<int64_t>(16, cdiv(T, 8 * P));
-        small = std::max<int64_t>(4, cdiv(T, 64 * P));
+    int32_t max_nblk = 1;
+    for (int32_t b = 0; b < B; ++b) {
+        nblks[b] = (int32_t)cdiv(lens[b], kv->d.block_size);
+        T += (int64_t)nblks[b] * Hkv;
+        max_nblk = std::max(max_nblk, nblks[b]);
     }
-    const int64_t pairs = std::max<int64_t>(1, (int64_t)B * Hkv);
-    const int64_t reserve = big == small ? 0 : cdiv(2 * P * small, pairs);
+    int64_t chunk;
+    bool latency = false;
+    if (kv->forced_chunk_blocks > 0) {
+        chunk = kv->forced_chunk_blocks;
+    } else if (T <= 64 * P) {
+        chunk = std::max<int64_t>(1, cdiv(T, P));
+        latency = true;
+    } else if (kv->plan_cache.valid && kv->plan_cache.B == B && kv->plan_cache.P == P &&
+               std::llabs(T - kv->plan_cache.T) * 50 <= kv->plan_cache.T) {
+        chunk = kv->plan_cache.chunk;
+    } else {
+        double best = 0;
+        chunk = max_nblk;
+        for (int64_t k : {0, 4, 6, 8, 12, 16, 24, 32}) {
+            const int64_t c = k == 0 ? max_nblk : std::max<int64_t>(4, cdiv(T, k * P));
+            if (k > 0 && c >= max_nblk) continue;
+            if ((int64_t)B * Hkv + T / c > kv->ws.max_items) continue;
+            const double cost = plan_cost(nblks, Hkv, c, P);
+            if (k == 0 || cost < best) {
+                best = cost;
+                chunk = k == 0 ? (int64_t)1 << 30 : c;     // "no split" stays no split as pairs grow
+            }
+        }
+        kv->plan_cache = {true, B, P, T, chunk};
+    }
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;
-    std::vector<int32_t> pieces;
+    std::vector<int32_t> pc;
     int32_t parts = 0;
     for (int32_t b = 0; b < B; ++b) {
-        const int32_t nblk = (int32_t)cdiv(lens[b], kv->d.block_size);
-        pieces.clear();
-        const int32_t nbig = big == small ? 0 : (int32_t)(std::max<int64_t>(0, nblk - reserve) / big);
-        for (int32_t i = 0; i < nbig; ++i) pieces.push_back((int32_t)big);
-        const int32_t rem = nblk - nbig * (int32_t)big;
-        const int32_t nsm = (int32_t)cdiv(rem, small);
-        for (int32_t i = 0; i < nsm; ++i) pieces.push_back(rem / nsm + (i < rem % nsm ? 1 : 0));
-        const bool split = pieces.size() > 1;
+        pieces_of(nblks[b], chunk, pc);
+        const bool split = pc.size() > 1;
         for (int32_t g = 0; g < Hkv; ++g) {
             const int32_t mg = split ? (int32_t)merges.size() : -1;
-            if (split) merges.push_back({b, g, parts, (int32_t)pieces.size()});
+            if (split) merges.push_back({b, g, parts, (int32_t)pc.size()});
             int32_t blk = 0;
-            for (size_t i = 0; i < pieces.size(); ++i) {
-                items.push_back({b, g, blk, pieces[i], split ? parts + (int32_t)i : -1, kv->batch_seq[b], lens[b], mg});
-                blk += pieces[i];
+            for (size_t i = 0; i < pc.size(); ++i) {
+                items.push_back({b, g, blk, pc[i], split ? parts + (int32_t)i : -1, kv->batch_seq[b], lens[b], mg});
+                blk += pc[i];
             }
-            if (split) parts += (int32_t)pieces.size();
+            if (split) parts += (int32_t)pc.size();
         }
     }
     if ((int64_t)items.size() > kv->ws.max_items)
         return fail(APEX_EINVAL, "split chunk of %lld tokens yields %zu work items > workspace capacity %d",
-                    (long long)small * kv->d.block_size, items.size(), kv->ws.max_items);
+                    (long long)chunk * kv->d.block_size, items.size(), kv->ws.max_items);
     std::stable_sort(items.begin(), items.end(),
                      [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
     kv->items.swap(items);
     kv->merges.swap(merges);
-    kv->fuse_merge = big == small && kv->forced_chunk_blocks == 0;   // latency regime: save the launch
+    kv->fuse_merge = latency;
+    kv->last_chunk = chunk;
     return APEX_OK;
 }
 

@@ -480,11 +480,27 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
+        // Control path (queue atomic -> item -> block-table entries) runs ahead
+        // of the TMA stream so no dependent global load sits between two tile
+        // issues: the queue slot of item k+2 is claimed when item k starts, item
+        // k+1 is loaded when item k starts, its first block-table chunk half-way
+        // through item k, and block-table chunk c+1 when chunk c starts.  Every
+        // claimed index < n_items is processed by the claiming CTA, in order.
         int32_t issued = 0;
+        auto bt_row = [&](const WorkItem &w) {
+            return p.block_table + (size_t)w.seq * p.max_blocks_per_seq + w.blk0;
+        };
+        int idx = 0, pend = 0;
+        if (lane == 0) idx = atomicAdd(p.counters, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (lane == 0) pend = atomicAdd(p.counters, 1);      // claim for item 1
+        WorkItem it{};
+        int my = 0;
+        if (idx < p.n_items) {
+            it = p.items[idx];
+            my = lane < it.nblk ? __ldg(bt_row(it) + lane) : 0;
+        }
         for (int k = 0;; ++k) {
-            int idx = 0;
-            if (lane == 0) idx = atomicAdd(p.counters, 1);
-            idx = __shfl_sync(0xffffffffu, idx, 0);
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
@@ -495,17 +511,24 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
-            const WorkItem it = p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
-            const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
+            const int nidx = __shfl_sync(0xffffffffu, pend, 0);   // claimed one item ago
+            WorkItem nit{};
+            if (nidx < p.n_items) nit = p.items[nidx];             // first used half-way through
+            if (lane == 0) pend = nidx < p.n_items ? atomicAdd(p.counters, 1) : p.n_items;
+            int nmy = 0;
+            bool nmy_loaded = false;
+            const int half = it.nblk >> 1;
+            const int32_t *bt = bt_row(it);
+            int t = 0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
+                const int my_next = (j0 + 32 + lane < it.nblk) ? __ldg(bt + j0 + 32 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
-                for (int jj = 0; jj < cnt; ++jj) {
+                for (int jj = 0; jj < cnt; ++jj, ++t) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
                     if (lane == 0) {
                         const int s = issued % STAGES, u = issued / STAGES;
@@ -525,8 +548,17 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                         }
                     }
                     ++issued;
+                    if (!nmy_loaded && t >= half) {
+                        nmy_loaded = true;
+                        if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
+                    }
                 }
+                my = my_next;
             }
+            if (!nmy_loaded && nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
+            idx = nidx;
+            it = nit;
+            my = nmy;
         }
         // last CTA out resets the queue for the next launch on this layer
         if (lane == 0) {

@@ -164,11 +164,9 @@ def test_planner_split_chunk_and_auto():
     assert nm == 8 and sum(1 for it in items if it[4] < 0) == 8
     c2 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024, max_new_tokens=1 << 20)
     c2.set_grid(296)
-    c2.alloc(list(range(4)), [16000] * 4)            # T = 32000 tiles > 64P: big 16 blocks, small 4
+    c2.alloc(list(range(4)), [16000] * 4)            # 32 pairs of 1000 blocks: must split (32 << 296 CTAs)
     items, nm = _check_plan(c2, [16000] * 4, 8)
-    # reserve ceil(2*296*4/32) = 74 blocks per pair for small pieces: 57 big (16) + 22 small (4)
-    assert len(items) == 32 * (57 + 22) and nm == 32
-    assert max(it[3] for it in items[-2 * 296:]) <= 4     # the queue tail holds only small pieces
+    assert len(items) >= 296 and nm == 32
     c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024)
     c3.set_grid(296)
     c3.alloc([0], [1000])                            # T = 63*8 = 504 <= 64P: ~1 item per CTA
@@ -207,3 +205,25 @@ def test_cost_model_spec_example_and_validation():
         with pytest.raises(A.ApexError) as ei:
             A.apex_cost_create(bg, kg, us)
         assert ei.value.code == "EINVAL"
+
+
+def test_planner_lpt_choice_at_config_scale():
+    import time
+    # C5-like: 8192 pairs of 1025 blocks on 296 CTAs -> no split is cheapest
+    c5 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=1024 * 1026, max_seqs=1024, max_blocks_per_seq=1100,
+                    max_batch=1024, max_new_tokens=1 << 24)
+    c5.set_grid(296)
+    c5.alloc(list(range(1024)), [16384] * 1024)
+    t0 = time.perf_counter()
+    c5.alloc(list(range(1024)), [1] * 1024)
+    dt = time.perf_counter() - t0
+    items, nm = c5.plan()
+    assert len(items) == 8192 and nm == 0
+    assert dt < 0.05                                 # cached choice: no re-simulation per step
+    # C3-like: 1024 pairs of 512 blocks (3.5 per CTA) -> split
+    c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=128 * 513, max_seqs=128, max_blocks_per_seq=520,
+                    max_batch=128, max_new_tokens=1 << 21)
+    c3.set_grid(296)
+    c3.alloc(list(range(128)), [8192] * 128)
+    items, nm = _check_plan(c3, [8192] * 128, 8)
+    assert len(items) >= 4 * 1024 and nm == 1024
