@@ -480,20 +480,21 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
-        // Control path (queue atomic -> item -> block-table entries) runs ahead
-        // of the TMA stream so no dependent global load sits between two tile
-        // issues: the queue slot of item k+2 is claimed when item k starts, item
-        // k+1 is loaded when item k starts, its first block-table chunk half-way
-        // through item k, and block-table chunk c+1 when chunk c starts.  Every
-        // claimed index < n_items is processed by the claiming CTA, in order.
+        // Control path (queue atomic -> item -> first block-table chunk) for
+        // item k+1 is started while the last tiles of item k are being issued
+        // (claim at <= 8 tiles left, item load at <= 5, block-table load at
+        // <= 2), so the dependent global loads overlap the ring instead of
+        // sitting between two tile issues.  The claim is late enough that the
+        // longest-first dynamic balance is preserved (a claimed index is always
+        // processed by its claimer, next).  Block-table chunk c+1 is loaded
+        // when chunk c starts.
         int32_t issued = 0;
         auto bt_row = [&](const WorkItem &w) {
             return p.block_table + (size_t)w.seq * p.max_blocks_per_seq + w.blk0;
         };
-        int idx = 0, pend = 0;
+        int idx = 0;
         if (lane == 0) idx = atomicAdd(p.counters, 1);
         idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (lane == 0) pend = atomicAdd(p.counters, 1);      // claim for item 1
         WorkItem it{};
         int my = 0;
         if (idx < p.n_items) {
@@ -516,13 +517,24 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
-            const int nidx = __shfl_sync(0xffffffffu, pend, 0);   // claimed one item ago
+            int nidx = 0, nmy = 0, stage = 0;   // stage: 0 none, 1 claimed, 2 item loading, 3 bt loading
             WorkItem nit{};
-            if (nidx < p.n_items) nit = p.items[nidx];             // first used half-way through
-            if (lane == 0) pend = nidx < p.n_items ? atomicAdd(p.counters, 1) : p.n_items;
-            int nmy = 0;
-            bool nmy_loaded = false;
-            const int half = it.nblk >> 1;
+            auto run_ahead = [&](int left) {
+                if (stage == 0 && left <= 8) {
+                    if (lane == 0) nidx = atomicAdd(p.counters, 1);
+                    stage = 1;
+                }
+                if (stage == 1 && left <= 5) {
+                    nidx = __shfl_sync(0xffffffffu, nidx, 0);
+                    if (nidx < p.n_items) nit = p.items[nidx];
+                    stage = 2;
+                }
+                if (stage == 2 && left <= 2) {
+                    if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
+                    stage = 3;
+                }
+            };
+            run_ahead(it.nblk);
             const int32_t *bt = bt_row(it);
             int t = 0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
@@ -548,14 +560,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                         }
                     }
                     ++issued;
-                    if (!nmy_loaded && t >= half) {
-                        nmy_loaded = true;
-                        if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
-                    }
+                    run_ahead(it.nblk - t - 1);
                 }
                 my = my_next;
             }
-            if (!nmy_loaded && nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
+            run_ahead(0);
             idx = nidx;
             it = nit;
             my = nmy;
