@@ -216,11 +216,6 @@ struct apex_kv {
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
     bool fuse_merge = false;
     int64_t last_chunk = 0;
-    struct {
-        bool valid;
-        int32_t B;
-        int64_t P, T, chunk;
-    } plan_cache{false, 0, 0, 0, 0};
 };
 
 extern "C" {
@@ -318,14 +313,12 @@ apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens) {
         return fail(APEX_EINVAL, "chunk_tokens %d must be a non-negative multiple of %d", chunk_tokens,
                     kv->d.block_size);
     kv->forced_chunk_blocks = chunk_tokens / kv->d.block_size;
-    kv->plan_cache.valid = false;
     return APEX_OK;
 }
 
 apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas) {
     if (!kv || ctas < 0) return fail(APEX_EINVAL, "bad grid override");
     kv->grid_override = ctas;
-    kv->plan_cache.valid = false;
     return APEX_OK;
 }
 
@@ -371,12 +364,9 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
 // the device queue (greedy LPT on P CTAs).
 //  * latency regime (T <= 64 P): chunk = ceil(T/P), about one item per CTA, and
 //    the LSE merge is fused into the decode kernel (saves a launch);
-//  * bandwidth regime: candidate chunks (no split, T/(kP) for k in 4..32) are
-//    scored by simulating the LPT schedule -- makespan in tiles + a per-item
-//    cost (~1 tile: item fetch/merge bookkeeping) + a fixed cost if a merge
-//    launch is needed -- and the cheapest wins.  The choice is cached and only
-//    re-evaluated when the batch or T changes by > 2% (the simulation is
-//    O(items log P) host work);
+//  * bandwidth regime: chunk = max(4, ceil(T/16P)) -- ~16 items per CTA keeps
+//    the LPT tail short while per-item costs stay ~1% (tools/tune.py sweeps);
+//    pairs shorter than the chunk stay whole (e.g. C5: no split at all);
 //  * a forced chunk (apex_kv_set_split) is used as is.
 // A pair cut into >1 pieces gets partial slots and a merge entry.
 namespace {
@@ -384,26 +374,6 @@ void pieces_of(int32_t nblk, int64_t chunk, std::vector<int32_t> &out) {
     out.clear();
     const int32_t n = (int32_t)cdiv(nblk, chunk);
     for (int32_t i = 0; i < n; ++i) out.push_back(nblk / n + (i < nblk % n ? 1 : 0));
-}
-
-// LPT makespan (tiles) of the item multiset produced by `chunk` + overheads
-double plan_cost(const std::vector<int32_t> &nblks, int32_t hkv, int64_t chunk, int64_t P) {
-    std::vector<int32_t> sizes, pc;
-    int64_t merges = 0;
-    for (int32_t nb : nblks) {
-        pieces_of(nb, chunk, pc);
-        if (pc.size() > 1) merges += hkv;
-        for (int32_t g = 0; g < hkv; ++g) sizes.insert(sizes.end(), pc.begin(), pc.end());
-    }
-    std::sort(sizes.begin(), sizes.end(), std::greater<int32_t>());
-    std::vector<int64_t> heap((size_t)P, 0);   // min-heap of CTA loads
-    for (int32_t sz : sizes) {
-        std::pop_heap(heap.begin(), heap.end(), std::greater<int64_t>());
-        heap.back() += sz + 1;                  // + ~1 tile of per-item cost
-        std::push_heap(heap.begin(), heap.end(), std::greater<int64_t>());
-    }
-    const int64_t makespan = *std::max_element(heap.begin(), heap.end());
-    return (double)makespan + (merges ? 12.0 + 2.0 * (double)merges / (double)P : 0.0);
 }
 }  // namespace
 
@@ -427,24 +397,10 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     } else if (T <= 64 * P) {
         chunk = std::max<int64_t>(1, cdiv(T, P));
         latency = true;
-    } else if (kv->plan_cache.valid && kv->plan_cache.B == B && kv->plan_cache.P == P &&
-               std::llabs(T - kv->plan_cache.T) * 50 <= kv->plan_cache.T) {
-        chunk = kv->plan_cache.chunk;
     } else {
-        double best = 0;
-        chunk = max_nblk;
-        for (int64_t k : {0, 4, 6, 8, 12, 16, 24, 32}) {
-            const int64_t c = k == 0 ? max_nblk : std::max<int64_t>(4, cdiv(T, k * P));
-            if (k > 0 && c >= max_nblk) continue;
-            if ((int64_t)B * Hkv + T / c > kv->ws.max_items) continue;
-            const double cost = plan_cost(nblks, Hkv, c, P);
-            if (k == 0 || cost < best) {
-                best = cost;
-                chunk = k == 0 ? (int64_t)1 << 30 : c;     // "no split" stays no split as pairs grow
-            }
-        }
-        kv->plan_cache = {true, B, P, T, chunk};
+        chunk = std::max<int64_t>(4, cdiv(T, 16 * P));
     }
+    (void)max_nblk;
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;
     std::vector<int32_t> pc;

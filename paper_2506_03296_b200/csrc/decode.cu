@@ -34,10 +34,19 @@
 namespace apex {
 namespace {
 
-constexpr int NC = 4;                    // consumer warps
+#ifndef APEX_NC
+#define APEX_NC 4
+#endif
+#ifndef APEX_CTAS_PER_SM
+#define APEX_CTAS_PER_SM 2
+#endif
+#ifndef APEX_L2_EVICT_FIRST
+#define APEX_L2_EVICT_FIRST 0
+#endif
+constexpr int NC = APEX_NC;              // consumer warps
 constexpr int NTHREADS = 32 * (NC + 1);
 constexpr int IR = 4;                    // item-ring entries
-constexpr int CTAS_PER_SM = 2;
+constexpr int CTAS_PER_SM = APEX_CTAS_PER_SM;
 constexpr int kTileRows = kBlock;        // 16 tokens per tile
 
 struct ItemSlot {
@@ -46,7 +55,7 @@ struct ItemSlot {
     int32_t pad[3];
 };
 
-constexpr int kSmemPerCta = 112640;      // 2 CTAs per SM fit the 228 KB SM carve-out
+constexpr int kSmemPerCta = (232448 - 1024 * CTAS_PER_SM) / CTAS_PER_SM - 1024;   // SM carve-out split
 
 template <int DT, int G> struct Cfg {
     static constexpr int ES = DT == APEX_F32 ? 4 : 2;
@@ -56,7 +65,7 @@ template <int DT, int G> struct Cfg {
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
     static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
-    static constexpr int STAGES = S0 > 12 ? 12 : S0;
+    static constexpr int STAGES = S0 > 24 ? 24 : S0;
     static constexpr int TILES = STAGES * 2 * TILE;
     static constexpr int BARS = (2 * STAGES + 2 * IR) * 8;
     static constexpr int TOTAL = TILES + BARS + RING + CB_O + CB_ML + 1024;   // + alignment slack
@@ -88,11 +97,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
                                             int c2) {
+#if APEX_L2_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+#else
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
             dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
     asm volatile(
@@ -480,28 +499,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
-        // Control path (queue atomic -> item -> first block-table chunk) for
-        // item k+1 is started while the last tiles of item k are being issued
-        // (claim at <= 8 tiles left, item load at <= 5, block-table load at
-        // <= 2), so the dependent global loads overlap the ring instead of
-        // sitting between two tile issues.  The claim is late enough that the
-        // longest-first dynamic balance is preserved (a claimed index is always
-        // processed by its claimer, next).  Block-table chunk c+1 is loaded
-        // when chunk c starts.
+        // (Measured: running the queue/item/block-table loads ahead of the TMA
+        // stream made this loop slower on B200 -- see DESIGN.md section 7.)
         int32_t issued = 0;
-        auto bt_row = [&](const WorkItem &w) {
-            return p.block_table + (size_t)w.seq * p.max_blocks_per_seq + w.blk0;
-        };
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(p.counters, 1);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        WorkItem it{};
-        int my = 0;
-        if (idx < p.n_items) {
-            it = p.items[idx];
-            my = lane < it.nblk ? __ldg(bt_row(it) + lane) : 0;
-        }
         for (int k = 0;; ++k) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.counters, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
@@ -512,35 +516,17 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
+            const WorkItem it = p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
-            int nidx = 0, nmy = 0, stage = 0;   // stage: 0 none, 1 claimed, 2 item loading, 3 bt loading
-            WorkItem nit{};
-            auto run_ahead = [&](int left) {
-                if (stage == 0 && left <= 8) {
-                    if (lane == 0) nidx = atomicAdd(p.counters, 1);
-                    stage = 1;
-                }
-                if (stage == 1 && left <= 5) {
-                    nidx = __shfl_sync(0xffffffffu, nidx, 0);
-                    if (nidx < p.n_items) nit = p.items[nidx];
-                    stage = 2;
-                }
-                if (stage == 2 && left <= 2) {
-                    if (nidx < p.n_items) nmy = lane < nit.nblk ? __ldg(bt_row(nit) + lane) : 0;
-                    stage = 3;
-                }
-            };
-            run_ahead(it.nblk);
-            const int32_t *bt = bt_row(it);
-            int t = 0;
+            const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my_next = (j0 + 32 + lane < it.nblk) ? __ldg(bt + j0 + 32 + lane) : 0;
+                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
-                for (int jj = 0; jj < cnt; ++jj, ++t) {
+                for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
                     if (lane == 0) {
                         const int s = issued % STAGES, u = issued / STAGES;
@@ -560,14 +546,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                         }
                     }
                     ++issued;
-                    run_ahead(it.nblk - t - 1);
                 }
-                my = my_next;
             }
-            run_ahead(0);
-            idx = nidx;
-            it = nit;
-            my = nmy;
         }
         // last CTA out resets the queue for the next launch on this layer
         if (lane == 0) {

@@ -207,7 +207,7 @@ def test_cost_model_spec_example_and_validation():
         assert ei.value.code == "EINVAL"
 
 
-def test_planner_lpt_choice_at_config_scale():
+def test_planner_choice_at_config_scale():
     import time
     # C5-like: 8192 pairs of 1025 blocks on 296 CTAs -> no split is cheapest
     c5 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=1024 * 1026, max_seqs=1024, max_blocks_per_seq=1100,
@@ -219,11 +219,11 @@ def test_planner_lpt_choice_at_config_scale():
     dt = time.perf_counter() - t0
     items, nm = c5.plan()
     assert len(items) == 8192 and nm == 0
-    assert dt < 0.05                                 # cached choice: no re-simulation per step
+    assert dt < 0.05                                 # per-step host planning stays cheap
     # C3-like: 1024 pairs of 512 blocks (3.5 per CTA) -> split
     c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=128 * 513, max_seqs=128, max_blocks_per_seq=520,
                     max_batch=128, max_new_tokens=1 << 21)
     c3.set_grid(296)
     c3.alloc(list(range(128)), [8192] * 128)
     items, nm = _check_plan(c3, [8192] * 128, 8)
-    assert len(items) >= 4 * 1024 and nm == 1024
+    assert len(items) == 5 * 1024 and nm == 1024     # chunk ceil(T/16P) = 111 blocks -> 5 pieces
