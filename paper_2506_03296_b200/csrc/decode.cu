@@ -499,17 +499,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
         }
-        // The producer loop is on the critical path at ~7 TB/s (one (block,
-        // head) tile pair every ~0.3 us per CTA), so the per-tile path is a
-        // lane-0-only loop: block ids come from a 32-entry shared buffer that the
-        // whole warp refills (next chunk prefetched into registers while lane 0
-        // issues), ring position is tracked incrementally, constants are hoisted.
-        // (Measured: running the queue/item loads ahead of the stream with early
-        // queue claims made it slower -- see DESIGN.md section 7.)
-        __shared__ int bt_buf[32];
-        int32_t issued = 0, s_idx = 0, s_round = 0;     // lane-0 ring position
-        const CUtensorMap *mk = &tmk, *mv = &tmv;
-        const int hkv = p.num_kv_heads, segs = p.tma_segs;
+        // (Measured alternatives -- control loads run ahead, lane-0-only tile loop,
+        // block-table chunk prefetch -- were all slower on B200.)
+        int32_t issued = 0;
         for (int k = 0;; ++k) {
             int idx = 0;
             if (lane == 0) idx = atomicAdd(p.counters, 1);
@@ -531,37 +523,30 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 mbar_arrive(ifull0 + 8 * slot);
             }
             const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
-            int my = lane < it.nblk ? __ldg(bt + lane) : 0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
+                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
-                bt_buf[lane] = my;
-                __syncwarp();
-                my = (j0 + 32 + lane < it.nblk) ? __ldg(bt + j0 + 32 + lane) : 0;   // next chunk, in flight
-                if (lane == 0) {
-                    const int gofs = it.g;
-                    for (int jj = 0; jj < cnt; ++jj) {
-                        const int row = (bt_buf[jj] * hkv + gofs) * kTileRows;
-                        if (s_round > 0) mbar_wait(empty0 + 8 * s_idx, (s_round - 1) & 1);
-                        const uint32_t bar = full0 + 8 * s_idx;
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const int phys = __shfl_sync(0xffffffffu, my, jj);
+                    if (lane == 0) {
+                        const int s = issued % STAGES, u = issued / STAGES;
+                        if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
+                        const uint32_t bar = full0 + 8 * s;
                         mbar_expect_tx(bar, 2 * TILE);
-                        const uint32_t dk = tiles_u + s_idx * 2 * TILE, dv = dk + TILE;
-                        if (segs == 1) {
-                            tma_load_3d(dk, mk, bar, 0, row, 0);
-                            tma_load_3d(dv, mv, bar, 0, row, 0);
+                        const int row = (phys * p.num_kv_heads + it.g) * kTileRows;
+                        const uint32_t dk = tiles_u + s * 2 * TILE, dv = dk + TILE;
+                        if (p.tma_segs == 1) {
+                            tma_load_3d(dk, &tmk, bar, 0, row, 0);
+                            tma_load_3d(dv, &tmv, bar, 0, row, 0);
                         } else {
-                            for (int sg = 0; sg < segs; ++sg) {
-                                tma_load_2d(dk + sg * 2048, mk, bar, sg * (128 / C::ES), row);
-                                tma_load_2d(dv + sg * 2048, mv, bar, sg * (128 / C::ES), row);
+                            for (int sg = 0; sg < p.tma_segs; ++sg) {
+                                tma_load_2d(dk + sg * 2048, &tmk, bar, sg * (128 / C::ES), row);
+                                tma_load_2d(dv + sg * 2048, &tmv, bar, sg * (128 / C::ES), row);
                             }
                         }
-                        ++issued;
-                        if (++s_idx == STAGES) {
-                            s_idx = 0;
-                            ++s_round;
-                        }
                     }
+                    ++issued;
                 }
-                __syncwarp();
             }
         }
         // last CTA out resets the queue for the next launch on this layer
