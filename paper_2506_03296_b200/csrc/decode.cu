@@ -460,7 +460,7 @@ __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeIte
 }
 
 // ------------------------------------------------------------------ decode kernel
-template <int DT, int G>
+template <int DT, int G, bool FUSE>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     apex_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                        const DecodeParams p) {
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (d4 == 0) *reinterpret_cast<float2 *>(p.part_ml + ((size_t)it.part * G + row) * 2) = make_float2(M, den);
                 }
             }
-            if (it.part >= 0 && p.fuse_merge) {
+            if (FUSE && it.part >= 0) {
                 // last-arriving split of this (b, g) pair merges all its partials (fused LSE merge)
                 __threadfence();
                 named_bar_sync(1, NC * 32);
@@ -636,14 +636,20 @@ __global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
 }
 
 template <int DT, int G> cudaError_t prepare() {
-    return cudaFuncSetAttribute(apex_decode_kernel<DT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(apex_decode_kernel<DT, G, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<DT, G>::TOTAL);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(apex_decode_kernel<DT, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Cfg<DT, G>::TOTAL);
 }
 
 template <int DT, int G>
 cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
     if (grid > 0) {
-        apex_decode_kernel<DT, G><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
+        if (p.fuse_merge)
+            apex_decode_kernel<DT, G, true><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
+        else
+            apex_decode_kernel<DT, G, false><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess || p.fuse_merge || p.n_merges == 0) return e;
     }
