@@ -11,10 +11,14 @@
 //  * warp 0 = producer: reads the block table 32 entries at a time and issues
 //    one TMA (cp.async.bulk.tensor, 128-B swizzle) per K and per V tile of a
 //    (block, kv-head) -- a contiguous 4 KiB (16-bit) / 8 KiB (fp32) tile --
-//    into a STAGES-deep mbarrier ring;
+//    into mbarrier-guarded shared-memory slots;
 //  * warps 1..4 = consumers: tile j of an item goes to consumer j % 4, each
 //    keeps its own running (m, l, O) and the four are merged through shared
-//    memory at the item's end (fixed order => deterministic);
+//    memory at the item's end (fixed order => deterministic).  Every consumer
+//    owns a private sub-ring of SW slots that it waits on strictly in order:
+//    with one shared ring a fast warp could wait on a slot whose previous fill
+//    was still in flight, and mbarrier try_wait.parity would report the
+//    preceding phase as complete (a race seen at C2 sizes);
 //  * GQA (g >= 2, 16-bit): S = Q_g K^T and O += P V on tensor cores with
 //    mma.sync.m16n8k16 (q-group rows padded to 16; P re-used from the S
 //    accumulator registers as the A operand), K/V fragments via ldmatrix on the
@@ -51,8 +55,7 @@ constexpr int kTileRows = kBlock;        // 16 tokens per tile
 
 struct ItemSlot {
     WorkItem it;
-    int32_t base;      // ring sequence number of the item's first tile
-    int32_t pad[3];
+    int32_t pad[4];
 };
 
 constexpr int kSmemPerCta = (232448 - 1024 * CTAS_PER_SM) / CTAS_PER_SM - 1024;   // SM carve-out split
@@ -65,12 +68,13 @@ template <int DT, int G> struct Cfg {
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
     static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
-    static constexpr int STAGES = S0 > 24 ? 24 : S0;
+    static constexpr int SW = (S0 > 24 ? 24 : S0) / NC;      // slots per consumer warp
+    static constexpr int STAGES = SW * NC;
     static constexpr int TILES = STAGES * 2 * TILE;
     static constexpr int BARS = (2 * STAGES + 2 * IR) * 8;
     static constexpr int TOTAL = TILES + BARS + RING + CB_O + CB_ML + 1024;   // + alignment slack
     static_assert(TOTAL <= kSmemPerCta, "shared memory budget");
-    static_assert(STAGES >= 4, "ring too shallow");
+    static_assert(SW >= 1, "ring too shallow");
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -501,7 +505,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         }
         // (Measured alternatives -- control loads run ahead, lane-0-only tile loop,
         // block-table chunk prefetch -- were all slower on B200.)
-        int32_t issued = 0;
+        int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
+#pragma unroll
+        for (int q = 0; q < NC; ++q) pc[q] = 0;
         for (int k = 0;; ++k) {
             int idx = 0;
             if (lane == 0) idx = atomicAdd(p.counters, 1);
@@ -519,7 +525,6 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             const WorkItem it = p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
-                ring[slot].base = issued;
                 mbar_arrive(ifull0 + 8 * slot);
             }
             const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
@@ -528,8 +533,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 const int cnt = min(32, it.nblk - j0);
                 for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
+                    const int w = (j0 + jj) % NC;
+                    int m = 0;
+#pragma unroll
+                    for (int q = 0; q < NC; ++q)
+                        if (q == w) m = pc[q]++;
                     if (lane == 0) {
-                        const int s = issued % STAGES, u = issued / STAGES;
+                        const int s = w * C::SW + m % C::SW, u = m / C::SW;
                         if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
                         const uint32_t bar = full0 + 8 * s;
                         mbar_expect_tx(bar, 2 * TILE);
@@ -545,7 +555,6 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                             }
                         }
                     }
-                    ++issued;
                 }
             }
         }
@@ -561,17 +570,18 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // ================= consumers =================
         const int wc = warp - 1;
         typename ConsumerSel<DT, G>::T st;
+        int32_t mc = 0;                       // tiles consumed from this warp's sub-ring
         for (int k = 0;; ++k) {
             const int slot = k % IR, use = k / IR;
             mbar_wait(ifull0 + 8 * slot, use & 1);
             const WorkItem it = ring[slot].it;
-            const int32_t base = ring[slot].base;
             __syncwarp();
             if (lane == 0) mbar_arrive(iempty0 + 8 * slot);
             if (it.nblk == 0) break;
             st.begin(p.q, p, it, lane);
             for (int j = wc; j < it.nblk; j += NC) {
-                const int n = base + j, s = n % STAGES, u = n / STAGES;
+                const int s = wc * C::SW + mc % C::SW, u = mc / C::SW;
+                ++mc;
                 mbar_wait(full0 + 8 * s, u & 1);
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;

@@ -171,3 +171,25 @@ def test_errors_and_unsupported(cuda_lib):
     with pytest.raises(A.ApexError) as e:
         cache.alloc([1], [16 * 8])
     assert e.value.code in ("ENOBLOCKS", "EINVAL")
+
+
+@pytest.mark.parametrize("dtype,hq,hkv,batch,ctx", [("f16", 32, 32, 16, 4096), ("bf16", 32, 8, 32, 8192),
+                                                   ("f32", 32, 32, 8, 4096)])
+def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
+    """Regression: with one shared tile ring, a fast consumer warp could pass a
+    try_wait.parity on a slot whose previous fill was still in flight (seen as a
+    launch failure at C2 sizes).  Repeated decodes of a bandwidth-regime shape."""
+    import torch
+    from helpers import gen_dev
+    cache = make_cache(dtype, hq, hkv, batch * (ctx // 16 + 2), max_seqs=batch, max_blocks_per_seq=ctx // 16 + 2)
+    seqs = list(range(batch))
+    prefill(cache, seqs, [ctx] * batch)
+    out = decode_step(cache, seqs, [ctx] * batch)
+    q = gen_dev(cache, 0, 0, seqs, [ctx - 1] * batch, hq)
+    for _ in range(20):
+        again = cache.decode(0, q)
+        torch.cuda.synchronize()
+        assert torch.equal(again, out)
+    rows = list(range(0, batch * hq, max(1, batch * hq // 64)))
+    ref = oracle_rows(seqs, [ctx] * batch, hq, hkv, dtype, rows=rows)
+    check_close(to_f64(out, dtype).reshape(-1, 128)[rows], ref, dtype)
