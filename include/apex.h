@@ -162,6 +162,41 @@ apex_status apex_predict_time(const apex_cost *cost, int32_t batch, int64_t kv_t
                               double *us_out);
 void apex_cost_destroy(apex_cost *cost);
 
+/* ---- APEX decision layer (§3.2 Eq1-Eq6, Algorithm 1) ---- */
+
+typedef enum {
+    APEX_STRATEGY_GPU_ONLY = 0,        /* Alg. 1: no CPU-decode requests (or ratio gate closed) */
+    APEX_STRATEGY_ASYM_PIPELINE = 1,   /* Asymmetric Pipelining (NEO) */
+    APEX_STRATEGY_ASYNC_OVERLAP = 2    /* Asynchronous Overlap */
+} apex_strategy;
+
+typedef struct {
+    int32_t n_prefill;        /* |P_sch| */
+    int32_t n_gpu_decode;     /* |D_gpu_sch| */
+    int32_t n_cpu_decode;     /* |D_cpu_sch| */
+    double n_g, n_c;          /* N_G, N_C: GPU / CPU attention rates, tokens per us */
+    double t_glinear;         /* T_glinear, us per layer (decode-only profile) */
+    double t_gatt;            /* T_gatt,   us per layer (decode-only profile) */
+    double t_glinear_pref;    /* T_glinear_pref (Alg. 1 mixed branch; ignored if n_prefill == 0) */
+    double t_gatt_pref;       /* T_gatt_pref */
+    double min_cpu_ratio;     /* CPU:GPU request-count gate (8); <= 0 disables the gate */
+} apex_sched_input;
+
+typedef struct {
+    apex_strategy strategy;
+    int32_t gate_closed;      /* 1 if the P:378 ratio gate forced GPU-only */
+    double lhs, rhs;          /* the two sides of the inequality evaluated (0 if none) */
+    double eq6_threshold;     /* 2 T_l/T_a + 3 + T_a/T_l (decode-only case), else 0 */
+} apex_decision;
+
+/* Eq6: AP beats GPU-only in decode-only batches iff N_G/N_C < this. */
+apex_status apex_pipelining_threshold(double t_glinear, double t_gatt, double *out);
+/* Algorithm 1 exactly as printed: GPU-only if no CPU-decode requests;
+   decode-only -> Eq5 decides AP vs AO; mixed -> the modified inequality with
+   T_overlap_with_prefill = T_glinear_pref + T_glinear + T_gatt_pref.  Pure host
+   function; APEX_EINVAL on non-positive times/rates or negative counts. */
+apex_status apex_decide(const apex_sched_input *in, apex_decision *out);
+
 /* Thread-local text for the last non-OK status of this thread ("" if none). */
 const char *apex_last_error(void);
 const char *apex_version(void);

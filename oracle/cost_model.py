@@ -59,3 +59,20 @@ def eq5_holds(n_g, n_c, t_glinear, t_gatt) -> bool:   # Eq5
 
 def eq6_threshold(t_glinear, t_gatt) -> float:        # Eq6
     return 2 * t_glinear / t_gatt + 3 + t_gatt / t_glinear
+
+
+def algorithm1(n_prefill, n_gpu, n_cpu, n_g, n_c, t_glinear, t_gatt, t_glinear_pref=None, t_gatt_pref=None,
+               min_cpu_ratio=8.0):
+    """Algorithm 1 step by step, plus the P:378 request-ratio gate (§4.2).
+
+    Returns "gpu_only" | "asym_pipeline" | "async_overlap"."""
+    if n_cpu == 0:                                          # lines 4-6
+        return "gpu_only"
+    if min_cpu_ratio and min_cpu_ratio > 0 and n_cpu < min_cpu_ratio * n_gpu:   # P:378
+        return "gpu_only"
+    if n_prefill == 0:                                      # lines 9-16 (decode-only, Eq5)
+        return "asym_pipeline" if eq5_holds(n_g, n_c, t_glinear, t_gatt) else "async_overlap"
+    t_overlap_with_prefill = t_glinear_pref + t_glinear + t_gatt_pref          # line 20
+    lhs = (n_g * t_gatt + n_c * t_overlap_with_prefill) / (2 * t_glinear + t_gatt)   # line 21
+    rhs = n_g * t_gatt / (t_glinear + t_gatt)
+    return "asym_pipeline" if lhs > rhs else "async_overlap"

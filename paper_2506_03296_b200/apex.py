@@ -25,7 +25,8 @@ EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex
            "apex_kv_append", "apex_decode_attention", "apex_kv_set_split", "apex_kv_set_grid",
            "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan",
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
-           "apex_synth_rows"]
+           "apex_synth_rows", "apex_pipelining_threshold", "apex_decide"]
+STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
 
 
 class ApexError(RuntimeError):
@@ -42,6 +43,17 @@ class apex_kv_desc(ctypes.Structure):
                 ("dtype", c_int), ("k_pool", POINTER(c_void_p)), ("v_pool", POINTER(c_void_p)),
                 ("block_table", c_void_p), ("seq_lens", c_void_p), ("workspace", c_void_p),
                 ("workspace_bytes", c_size_t)]
+
+
+class apex_sched_input(ctypes.Structure):
+    _fields_ = [("n_prefill", c_int32), ("n_gpu_decode", c_int32), ("n_cpu_decode", c_int32), ("n_g", c_double),
+                ("n_c", c_double), ("t_glinear", c_double), ("t_gatt", c_double), ("t_glinear_pref", c_double),
+                ("t_gatt_pref", c_double), ("min_cpu_ratio", c_double)]
+
+
+class apex_decision(ctypes.Structure):
+    _fields_ = [("strategy", c_int), ("gate_closed", c_int32), ("lhs", c_double), ("rhs", c_double),
+                ("eq6_threshold", c_double)]
 
 
 _lib = None
@@ -77,6 +89,8 @@ def lib():
             "apex_version": (c_char_p, []),
             "apex_synth_rows": (c_int, [c_void_p, c_int, c_int32, c_int32, c_void_p, c_void_p, c_int64, c_int32,
                                         c_int32, c_int32, c_uint64, c_float, c_void_p]),
+            "apex_pipelining_threshold": (c_int, [c_double, c_double, POINTER(c_double)]),
+            "apex_decide": (c_int, [POINTER(apex_sched_input), POINTER(apex_decision)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -196,3 +210,24 @@ def apex_synth_rows(out_ptr: int, dtype: str, tensor: int, layer: int, row_b_ptr
                     stream: int = 0) -> None:
     _check(lib().apex_synth_rows(out_ptr, DTYPE_CODE[dtype], tensor, layer, row_b_ptr, row_pos_ptr, n_rows,
                                  n_heads, head_offset, head_dim, seed, amp, stream))
+
+
+def apex_pipelining_threshold(t_glinear: float, t_gatt: float) -> float:
+    out = c_double()
+    st = lib().apex_pipelining_threshold(float(t_glinear), float(t_gatt), ctypes.byref(out))
+    if st != APEX_OK:
+        raise ApexError(st, "apex_pipelining_threshold: times must be finite and > 0")
+    return out.value
+
+
+def apex_decide(n_prefill: int, n_gpu_decode: int, n_cpu_decode: int, n_g: float, n_c: float, t_glinear: float,
+                t_gatt: float, t_glinear_pref: float = 0.0, t_gatt_pref: float = 0.0, min_cpu_ratio: float = 8.0):
+    """Algorithm 1 decision -> dict(strategy, gate_closed, lhs, rhs, eq6_threshold)."""
+    inp = apex_sched_input(n_prefill, n_gpu_decode, n_cpu_decode, n_g, n_c, t_glinear, t_gatt, t_glinear_pref,
+                           t_gatt_pref, min_cpu_ratio)
+    out = apex_decision()
+    st = lib().apex_decide(ctypes.byref(inp), ctypes.byref(out))
+    if st != APEX_OK:
+        raise ApexError(st, "apex_decide: invalid input")
+    return {"strategy": STRATEGIES[out.strategy], "gate_closed": bool(out.gate_closed), "lhs": out.lhs,
+            "rhs": out.rhs, "eq6_threshold": out.eq6_threshold}
