@@ -509,9 +509,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 #pragma unroll
         for (int q = 0; q < NC; ++q) pc[q] = 0;
         for (int k = 0;; ++k) {
-            int idx = 0;
-            if (lane == 0) idx = atomicAdd(p.counters, 1);
-            idx = __shfl_sync(0xffffffffu, idx, 0);
+            // first item is static (CTA i takes item i: no queue round trip on the
+            // launch-latency path); later items come from the queue, offset by grid
+            int idx = blockIdx.x;
+            if (k > 0) {
+                if (lane == 0) idx = (int)gridDim.x + atomicAdd(p.counters, 1);
+                idx = __shfl_sync(0xffffffffu, idx, 0);
+            }
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
