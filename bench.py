@@ -372,6 +372,7 @@ def run_apex(args):
     for s in range(W):
         step(s)
     n_items, n_merges = len(cache.plan()[0]), cache.plan()[1]
+    decode_launches = cache.decode_launches()
     clocks = ClockSampler(local) if rank == 0 else None
     barrier()
     torch.cuda.synchronize()
@@ -422,7 +423,7 @@ def run_apex(args):
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
-              "gpu_launches": K * (1 + 2 * L),     # apply-deltas + L x (append, decode)
+              "gpu_launches": K * (1 + L * (1 + decode_launches)),   # deltas + L x (append, decode[, merge])
               "prefill_s": t_fill}
     if clk:
         result["clocks"] = clk

@@ -149,6 +149,11 @@ apex_status apex_kv_last_slots(const apex_kv *kv, int32_t *slots, int32_t cap, i
 apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t *n_items,
                          int32_t *n_merges);
 
+/* Kernel launches the next apex_decode_attention will issue for the last alloc's
+   plan: 1 (decode kernel; unsplit or merge fused in-kernel) or 2 (+ merge kernel).
+   Returns -1 if no step is allocated. */
+int32_t apex_kv_decode_launches(const apex_kv *kv);
+
 /* ---- profiling-informed time prediction ---- */
 
 /* Table of measured per-layer-call decode-attention times us[i*nk + j] at

@@ -324,6 +324,11 @@ apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas) {
 
 int32_t apex_kv_num_free_blocks(const apex_kv *kv) { return kv ? (int32_t)kv->free_stack.size() : -1; }
 
+int32_t apex_kv_decode_launches(const apex_kv *kv) {
+    if (!kv || !kv->have_step) return -1;
+    return (!kv->merges.empty() && !kv->fuse_merge) ? 2 : 1;
+}
+
 apex_status apex_kv_seq_info(const apex_kv *kv, int32_t seq_id, int32_t *len, int32_t *blocks, int32_t cap,
                              int32_t *n_blocks) {
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");

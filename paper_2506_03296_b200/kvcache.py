@@ -132,6 +132,10 @@ class PagedKVCache:
     def plan(self):
         return A.apex_kv_plan(self.handle)
 
+    def decode_launches(self) -> int:
+        """Kernel launches the next decode() issues (1, or 2 with the merge kernel)."""
+        return A.apex_kv_decode_launches(self.handle)
+
 
 def synth_rows(out, dtype: str, tensor: int, layer: int, row_b, row_pos, head_offset: int = 0, seed: int = 0,
                amp: float = 1.0):

@@ -169,9 +169,12 @@ def test_planner_split_chunk_and_auto():
     assert len(items) >= 296 and nm == 32
     c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024)
     c3.set_grid(296)
+    assert A.apex_kv_decode_launches(c3.handle) == -1
     c3.alloc([0], [1000])                            # T = 63*8 = 504 <= 64P: ~1 item per CTA
     items, nm = _check_plan(c3, [1000], 8)
     assert len(items) == 8 * 32 and all(it[3] == 2 for it in items[:-8])
+    assert c3.decode_launches() == 1                 # latency regime: merge fused in-kernel
+    assert c2.decode_launches() == 2                 # bandwidth regime with splits: + merge kernel
     with pytest.raises(A.ApexError):
         c2.set_split(10)                             # not a multiple of 16
 
