@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo + APEX_BENCH_SAME_DEVICE=1 runs several ranks on one GPU (logic test only)")
     return ap.parse_args()
 
 
@@ -272,10 +274,17 @@ def run_apex(args):
     from paper_2506_03296_b200.kvcache import PagedKVCache, synth_rows, torch_dtype
 
     rank, world, local = dist_env()
+    if os.environ.get("APEX_BENCH_SAME_DEVICE") == "1":
+        local = 0                                     # test mode: several ranks share GPU 0 (gloo only)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    gloo = args.dist_backend == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll_dev = torch.device("cpu") if gloo else dev   # where small reduction tensors live
     w = WORKLOADS[args.config]
     wl = rank_workload(w, rank, world, args.mode)
     ids, ctx0 = wl["ids"], np.asarray(wl["ctx"], dtype=np.int64)
@@ -356,7 +365,7 @@ def run_apex(args):
             if timed_idx is not None:
                 ev[timed_idx * L + l][1].record()
             if head_mode:
-                gathered[p] = gather_heads(outs[p])
+                gathered[p] = gather_heads(outs[p]) if not gloo else gather_heads(outs[p].cpu())
 
     def barrier():
         if world > 1:
@@ -365,7 +374,7 @@ def run_apex(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -398,7 +407,7 @@ def run_apex(args):
     peak, peak_src = measured_peak()
     total_tokens = B * K
     if world > 1:
-        tt = torch.tensor([float(B * K)], dtype=torch.float64, device=dev)
+        tt = torch.tensor([float(B * K)], dtype=torch.float64, device=coll_dev)
         if wl["parallelism"].startswith("head"):
             tt /= world                               # every rank serves the same requests
         dist.all_reduce(tt)
@@ -419,7 +428,8 @@ def run_apex(args):
               "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,
               "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                            "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.config),
-                           "kernel": "apex_decode_attention (apex_decode_kernel, fused split-KV + LSE merge)",
+                           "kernel": "apex_decode_attention = apex_decode_kernel (+ apex_merge_kernel when split "
+                                     "pairs are merged in a second launch)",
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
@@ -447,6 +457,20 @@ def run_apex(args):
         result["cpu_baseline"] = {"value": cpu_tok_s, "unit": UNIT, "cores": cores, "kind": "oracle",
                                   "sample": desc, "oracle_seconds": t_or,
                                   "cpu": _cpu_model()}
+    elif rank == 0 and world > 1 and not args.no_cpu:
+        # sampled parity of this rank's rows (request sharding) or of the all-gathered
+        # full-head output (head sharding) against the oracle over all global heads
+        p_last = (L - 1) % P
+        ctx_now = ctx0 + (W + K - 1)
+        full_wl = dict(wl, hq=w.num_q_heads, hkv=w.num_kv_heads, q_off=0, kv_off=0)
+        sampler = OracleSampler(w, full_wl, p_last, args.seed, dt, ctx_now)
+        _, _, o_ref = sampler.run(ctx_now, 0.0, max_requests=2)
+        got_t = gathered[p_last] if head_mode else outs[p_last]
+        got = got_t.to(torch.float64).cpu().numpy()
+        errs = [float(np.abs(got[i] - o_ref[i]).max()) for i in o_ref]
+        result["parity_sample"] = {"requests": sorted(int(wl["ids"][i]) for i in o_ref),
+                                   "rows": len(o_ref) * w.num_q_heads, "max_abs_err": max(errs),
+                                   "checked": "all-gathered heads" if head_mode else "rank-0 requests"}
     # ---- end-to-end leg: host (pinned) inputs -> C ABI -> host outputs, every step
     if not args.no_e2e:
         qh = [torch.empty((B, hq, D), dtype=tdt, pin_memory=True) for _ in range(P)]
@@ -486,7 +510,7 @@ def run_apex(args):
                 cache.append(p, kd[j], vd[j])
                 cache.decode(p, qd[j], out=od[j])
                 if head_mode:
-                    oh[p] = gather_heads(od[j]).cpu()
+                    oh[p] = gather_heads(od[j] if not gloo else od[j].cpu()).cpu()
                     buf_free[j].record(comp)
                     continue
                 dec_done[j].record(comp)
