@@ -494,15 +494,18 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             mbar_init(iempty0 + 8 * i, NC);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
     }
     __syncthreads();
+    // PDL: everything above overlapped the previous kernel; from here on we read
+    // its results (pools, block table, lengths).  Dependents (the merge kernel)
+    // may be scheduled now; they wait on their own griddepcontrol.wait.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ================= producer: work queue + block table + TMA =================
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
-        }
         // (Measured alternatives -- control loads run ahead, lane-0-only tile loop,
         // block-table chunk prefetch -- were all slower on B200.)
         int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
@@ -646,6 +649,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 // per (b, g) pair, so merging never stalls a decode CTA's TMA stream.
 template <int DT, int G>
 __global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
     merge_pair<DT, G>(p, p.merges[blockIdx.x], threadIdx.x, blockDim.x);
 }
 
@@ -657,20 +661,36 @@ template <int DT, int G> cudaError_t prepare() {
                                 Cfg<DT, G>::TOTAL);
 }
 
+// Decode and merge kernels are launched with programmatic dependent launch:
+// their prologue (barrier init, descriptor prefetch) overlaps the tail of the
+// previous kernel on the stream, and griddepcontrol.wait orders every read of
+// the previous kernel's results.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int DT, int G>
 cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
     if (grid > 0) {
-        if (p.fuse_merge)
-            apex_decode_kernel<DT, G, true><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
-        else
-            apex_decode_kernel<DT, G, false><<<grid, NTHREADS, Cfg<DT, G>::TOTAL, s>>>(tm.k, tm.v, p);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = p.fuse_merge
+                            ? launch_pdl(apex_decode_kernel<DT, G, true>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.k,
+                                         tm.v, p)
+                            : launch_pdl(apex_decode_kernel<DT, G, false>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s,
+                                         tm.k, tm.v, p);
         if (e != cudaSuccess || p.fuse_merge || p.n_merges == 0) return e;
     }
-    if (p.n_merges > 0) {
-        apex_merge_kernel<DT, G><<<p.n_merges, 128, 0, s>>>(p);
-        return cudaGetLastError();
-    }
+    if (p.n_merges > 0) return launch_pdl(apex_merge_kernel<DT, G>, p.n_merges, 128, 0, s, p);
     return cudaSuccess;
 }
 
