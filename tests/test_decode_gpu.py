@@ -193,3 +193,44 @@ def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
     rows = list(range(0, batch * hq, max(1, batch * hq // 64)))
     ref = oracle_rows(seqs, [ctx] * batch, hq, hkv, dtype, rows=rows)
     check_close(to_f64(out, dtype).reshape(-1, 128)[rows], ref, dtype)
+
+
+def test_randomized_shapes_and_splits(cuda_lib):
+    """Seeded sweep: random dtype/group, ragged lengths, forced or automatic splits."""
+    rng = np.random.default_rng(1234)
+    combos = COMBOS + [("bf16", 64, 8), ("f16", 32, 4)]
+    for case in range(16):
+        dtype, hq, hkv = combos[rng.integers(len(combos))]
+        ctx = [int(x) for x in rng.integers(1, 3000, size=int(rng.integers(1, 9)))]
+        split = [None, 16, 48, 256, 1024][int(rng.integers(5))]
+        qamp = float(2 ** int(rng.integers(0, 4)))
+        _, seqs, out = run_case(dtype, hq, hkv, ctx, split=split, interleave=int(rng.integers(0, 40)),
+                                seed=case, qamp=qamp)
+        ref = oracle_rows(seqs, ctx, hq, hkv, dtype, seed=case, qamp=qamp)
+        check_close(out, ref, dtype)
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_small(cuda_lib, tool, tmp_path):
+    """compute-sanitizer on a small decode (split + merge + fused-merge paths): 0 errors."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "case.py"
+    script.write_text(
+        "import sys\n"
+        f"sys.path.insert(0, {root!r}); sys.path.insert(0, {os.path.join(root, 'tests')!r})\n"
+        "import torch\n"
+        "from helpers import make_cache, prefill, decode_step\n"
+        "for dtype, hq, hkv, split in (('bf16', 16, 4, 64), ('f16', 4, 4, None), ('f32', 4, 4, 32)):\n"
+        "    c = make_cache(dtype, hq, hkv, 64, max_seqs=4, max_blocks_per_seq=20)\n"
+        "    if split: c.set_split(split)\n"
+        "    prefill(c, [0, 1, 2], [1, 100, 257])\n"
+        "    decode_step(c, [0, 1, 2], [1, 100, 257])\n"
+        "    torch.cuda.synchronize()\n"
+        "print('done')\n")
+    r = subprocess.run(["compute-sanitizer", "--tool", tool, "--error-exitcode", "9", sys.executable, str(script)],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "done" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
