@@ -233,4 +233,5 @@ def test_compute_sanitizer_small(cuda_lib, tool, tmp_path):
     r = subprocess.run(["compute-sanitizer", "--tool", tool, "--error-exitcode", "9", sys.executable, str(script)],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "done" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
-    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
+    summary = r.stdout + r.stderr
+    assert "ERROR SUMMARY: 0 errors" in summary or "(0 errors, 0 warnings)" in summary, summary[-2000:]
