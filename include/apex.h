@@ -25,6 +25,12 @@
  *     (or ordered by the caller): apex_kv_alloc uploads the step's metadata into
  *     the workspace that apex_kv_append / apex_decode_attention read.
  *   - A handle is not thread-safe; use one handle per (process, GPU, model).
+ *   - CUDA graphs: every launch made by apex_kv_append / apex_decode_attention
+ *     has step-invariant parameters (the step's counts are read from a device
+ *     header that apex_kv_alloc uploads; grids and workspace offsets are fixed),
+ *     so the per-layer calls may be captured once and replayed every step with
+ *     apex_kv_alloc called outside the graph before each replay.  q/out/k_new/
+ *     v_new must then be the same (static) buffers at every replay.
  *   - Host-only handles (desc.k_pool == NULL and desc.block_table == NULL) run
  *     the allocator and planner without any CUDA call; append/decode then
  *     return APEX_EINVAL.  Used by CPU tests and host-side planning.
@@ -150,8 +156,9 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
                          int32_t *n_merges);
 
 /* Kernel launches the next apex_decode_attention will issue for the last alloc's
-   plan: 1 (decode kernel; unsplit or merge fused in-kernel) or 2 (+ merge kernel).
-   Returns -1 if no step is allocated. */
+   plan: 1 (decode kernel; LSE merge fused in-kernel, latency regime) or 2
+   (decode kernel + merge kernel; the merge kernel exits at once if the step has
+   no split pairs).  Returns -1 if no step is allocated. */
 int32_t apex_kv_decode_launches(const apex_kv *kv);
 
 /* ---- profiling-informed time prediction ---- */

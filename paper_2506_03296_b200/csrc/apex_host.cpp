@@ -66,6 +66,7 @@ int query_sm_count(bool host_only) {
 struct WsLayout {
     int32_t max_items = 0, max_merges = 0, max_bt_delta = 0;
     size_t counters = 0, merge_counters = 0, upload = 0, upload_cap = 0, part_o = 0, part_ml = 0, total = 0;
+    size_t o_items = 0, o_merges = 0, o_tail = 0;             // offsets inside the upload region
 };
 
 WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
@@ -76,9 +77,12 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     w.max_items = (int32_t)std::min<int64_t>(pairs + 64LL * 4 * sm_count + 64, 1 << 24);
     w.max_merges = (int32_t)pairs;
     w.max_bt_delta = (int32_t)(cdiv(d->max_new_tokens, d->block_size) + d->max_batch);
-    size_t up = 0;
-    up += align_up(sizeof(WorkItem) * (size_t)w.max_items, 256);
-    up += align_up(sizeof(MergeItem) * (size_t)w.max_merges, 256);
+    // upload region, fixed offsets: [StepHeader | work items | merges | tail: slots,
+    // block-table deltas, length deltas (packed)]; the kernels' pointers into it never move
+    w.o_items = 256;
+    w.o_merges = w.o_items + align_up(sizeof(WorkItem) * (size_t)w.max_items, 256);
+    w.o_tail = w.o_merges + align_up(sizeof(MergeItem) * (size_t)w.max_merges, 256);
+    size_t up = w.o_tail;
     up += align_up(sizeof(int32_t) * (size_t)d->max_new_tokens, 256);
     up += align_up(sizeof(int2) * (size_t)w.max_bt_delta, 256);
     up += align_up(sizeof(int2) * (size_t)d->max_batch, 256);
@@ -202,9 +206,6 @@ struct apex_kv {
     std::vector<int32_t> batch_seq, slots;
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;
-    const WorkItem *d_items = nullptr;
-    const MergeItem *d_merges = nullptr;
-    const int32_t *d_slots = nullptr;
 
     // pinned staging ring for the per-step upload
     uint8_t *staging[2] = {nullptr, nullptr};
@@ -326,7 +327,7 @@ int32_t apex_kv_num_free_blocks(const apex_kv *kv) { return kv ? (int32_t)kv->fr
 
 int32_t apex_kv_decode_launches(const apex_kv *kv) {
     if (!kv || !kv->have_step) return -1;
-    return (!kv->merges.empty() && !kv->fuse_merge) ? 2 : 1;
+    return kv->fuse_merge ? 1 : 2;
 }
 
 apex_status apex_kv_seq_info(const apex_kv *kv, int32_t seq_id, int32_t *len, int32_t *blocks, int32_t cap,
@@ -508,27 +509,34 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         kv->staged_pending[r] = false;
     }
     uint8_t *host = kv->staging[r];
-    size_t off = 0;
+    const apex::StepHeader hdr{(int32_t)kv->items.size(), (int32_t)kv->merges.size(), (int32_t)rows, 0};
+    std::memcpy(host, &hdr, sizeof hdr);
+    const size_t items_bytes = sizeof(WorkItem) * kv->items.size();
+    const size_t merges_bytes = sizeof(MergeItem) * kv->merges.size();
+    std::memcpy(host + kv->ws.o_items, kv->items.data(), items_bytes);
+    if (merges_bytes) std::memcpy(host + kv->ws.o_merges, kv->merges.data(), merges_bytes);
+    size_t off = kv->ws.o_tail;
     auto put = [&](const void *src, size_t bytes) {
         const size_t at = off;
         if (bytes) std::memcpy(host + at, src, bytes);
         off = align_up(off + bytes, 256);
         return at;
     };
-    const size_t o_items = put(kv->items.data(), sizeof(WorkItem) * kv->items.size());
-    const size_t o_merges = put(kv->merges.data(), sizeof(MergeItem) * kv->merges.size());
-    const size_t o_slots = put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
+    put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
     const size_t o_bt = put(bt_delta.data(), sizeof(int2) * bt_delta.size());
     const size_t o_len = put(len_delta.data(), sizeof(int2) * len_delta.size());
     uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, s);
+    // header + items | merges | tail: three copies of exactly the used bytes
+    cudaError_t e = cudaMemcpyAsync(dev, host, kv->ws.o_items + items_bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && merges_bytes)
+        e = cudaMemcpyAsync(dev + kv->ws.o_merges, host + kv->ws.o_merges, merges_bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dev + kv->ws.o_tail, host + kv->ws.o_tail, off - kv->ws.o_tail, cudaMemcpyHostToDevice,
+                            s);
     if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
     if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: metadata upload");
     kv->staged_pending[r] = true;
-    kv->d_items = (const WorkItem *)(dev + o_items);
-    kv->d_merges = (const MergeItem *)(dev + o_merges);
-    kv->d_slots = (const int32_t *)(dev + o_slots);
     e = apex::launch_apply_deltas((const int2 *)(dev + o_bt), (int)bt_delta.size(), (const int2 *)(dev + o_len),
                                   (int)len_delta.size(), kv->d.block_table, kv->d.seq_lens, s);
     if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: apply deltas");
@@ -550,11 +558,13 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
     if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
     if (!kv->have_step) return fail(APEX_EINVAL, "apex_kv_append before apex_kv_alloc");
     if (layer < 0 || layer >= kv->d.num_layers) return fail(APEX_EINVAL, "layer %d out of range", layer);
-    if (kv->n_rows == 0) return APEX_OK;
-    if (!k_new || !v_new) return fail(APEX_EINVAL, "k_new/v_new is NULL");
+    if (kv->n_rows > 0 && (!k_new || !v_new)) return fail(APEX_EINVAL, "k_new/v_new is NULL");
     if (((uintptr_t)k_new | (uintptr_t)v_new) & 15) return fail(APEX_EINVAL, "k_new/v_new not 16-byte aligned");
+    // always one launch (it reads the row count from the step header): graph-capturable
+    uint8_t *up = (uint8_t *)kv->d.workspace + kv->ws.upload;
     cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->k_pools[layer], kv->v_pools[layer],
-                                        kv->d_slots, kv->n_rows, kv->d.num_kv_heads, (cudaStream_t)stream);
+                                        (const int32_t *)(up + kv->ws.o_tail), (const apex::StepHeader *)up,
+                                        kv->d.num_kv_heads, kv->sm_count, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_kv_append");
 }
 
@@ -571,22 +581,25 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
     p.q = q;
     p.out = out;
     p.block_table = kv->d.block_table;
-    p.items = kv->d_items;
-    p.merges = kv->d_merges;
     uint8_t *ws = (uint8_t *)kv->d.workspace;
+    uint8_t *up = ws + kv->ws.upload;
+    p.hdr = (const apex::StepHeader *)up;
+    p.items = (const WorkItem *)(up + kv->ws.o_items);
+    p.merges = (const MergeItem *)(up + kv->ws.o_merges);
     p.part_o = (float *)(ws + kv->ws.part_o);
     p.part_ml = (float *)(ws + kv->ws.part_ml);
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
     p.merge_counters = (int32_t *)(ws + kv->ws.merge_counters);
-    p.n_items = (int32_t)kv->items.size();
-    p.n_merges = (int32_t)kv->merges.size();
+    p.merge_grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kv->ws.max_merges, 2LL * kv->sm_count));
     p.max_blocks_per_seq = kv->d.max_blocks_per_seq;
     p.num_q_heads = kv->d.num_q_heads;
     p.num_kv_heads = kv->d.num_kv_heads;
     p.scale_log2 = (float)((double)scale * 1.4426950408889634);   // log2(e)
     p.tma_segs = kv->tma_segs;
     p.fuse_merge = kv->fuse_merge ? 1 : 0;
-    const int grid = std::min<int>(p.n_items, apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
+    // fixed persistent grid (CTAs without an item exit at once): every launch parameter is
+    // step-invariant, so the per-layer launches can be captured in a CUDA graph
+    const int grid = apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count);
     cudaError_t e = apex::launch_decode(kv->d.dtype, kv->group, kv->tmaps[layer], p, grid, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_decode_attention");
 }

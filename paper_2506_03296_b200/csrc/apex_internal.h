@@ -33,6 +33,18 @@ struct __align__(16) MergeItem {
     int32_t b, g, part0, nparts;
 };
 
+// Per-step counts, uploaded with the work list.  Kernels read them from device
+// memory so every launch of apex_kv_append / apex_decode_attention has
+// step-invariant parameters (fixed pointers, fixed grids): a captured CUDA graph
+// of the per-layer launches stays valid across steps; only apex_kv_alloc (host
+// planning + H2D upload) runs outside the graph.
+struct __align__(16) StepHeader {
+    int32_t n_items;
+    int32_t n_merges;
+    int32_t n_rows;       // new-token rows of the step (append)
+    int32_t pad;
+};
+
 struct DecodeParams {
     const void *q;             // [B][Hq][D]
     void *out;                 // [B][Hq][D]
@@ -43,8 +55,8 @@ struct DecodeParams {
     float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)
     int32_t *counters;         // [2]: work-queue head, CTAs done
     int32_t *merge_counters;   // [n_merges]: split items finished per pair (left at 0)
-    int32_t n_items;
-    int32_t n_merges;
+    const StepHeader *hdr;     // this step's counts (device, written by apex_kv_alloc's upload)
+    int32_t merge_grid;        // fixed grid of the merge kernel (grid-stride over hdr->n_merges)
     int32_t max_blocks_per_seq;
     int32_t num_q_heads;
     int32_t num_kv_heads;
@@ -62,8 +74,8 @@ struct TmaPair {
 cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
                                 int32_t *block_table, int32_t *seq_lens, cudaStream_t s);
 cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool,
-                          void *v_pool, const int32_t *slots, int n_rows, int n_kv_heads,
-                          cudaStream_t s);
+                          void *v_pool, const int32_t *slots, const StepHeader *hdr, int n_kv_heads,
+                          int sm_count, cudaStream_t s);
 cudaError_t launch_decode(apex_dtype dt, int group, const TmaPair &tm, const DecodeParams &p,
                           int grid, cudaStream_t s);
 // persistent-grid size the decode kernel of (dtype, group) runs with on this device

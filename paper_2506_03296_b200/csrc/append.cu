@@ -13,8 +13,10 @@ namespace {
 __global__ void __launch_bounds__(256) apex_append_kernel(const uint4 *__restrict__ k_new,
                                                           const uint4 *__restrict__ v_new, uint4 *__restrict__ k_pool,
                                                           uint4 *__restrict__ v_pool,
-                                                          const int32_t *__restrict__ slots, int n_rows, int hkv,
+                                                          const int32_t *__restrict__ slots,
+                                                          const StepHeader *__restrict__ hdr, int hkv,
                                                           int chunks_per_vec) {
+    const int n_rows = hdr->n_rows;                       // step count from the device header
     const int64_t per_tensor = (int64_t)n_rows * hkv * chunks_per_vec;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * per_tensor; i += stride) {
@@ -59,17 +61,15 @@ cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_
     return cudaGetLastError();
 }
 
+// Fixed grid (grid-stride over hdr->n_rows) so the launch is step-invariant.
 cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool, void *v_pool,
-                          const int32_t *slots, int n_rows, int n_kv_heads, cudaStream_t s) {
-    if (n_rows <= 0) return cudaSuccess;
+                          const int32_t *slots, const StepHeader *hdr, int n_kv_heads, int sm_count,
+                          cudaStream_t s) {
     const int es = dt == APEX_F32 ? 4 : 2;
     const int cpv = kHeadDim * es / 16;
-    const int64_t total = 2LL * n_rows * n_kv_heads * cpv;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    apex_append_kernel<<<(int)blocks, 256, 0, s>>>(static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new),
-                                                   static_cast<uint4 *>(k_pool), static_cast<uint4 *>(v_pool), slots,
-                                                   n_rows, n_kv_heads, cpv);
+    apex_append_kernel<<<sm_count * 8, 256, 0, s>>>(static_cast<const uint4 *>(k_new),
+                                                    static_cast<const uint4 *>(v_new), static_cast<uint4 *>(k_pool),
+                                                    static_cast<uint4 *>(v_pool), slots, hdr, n_kv_heads, cpv);
     return cudaGetLastError();
 }
 

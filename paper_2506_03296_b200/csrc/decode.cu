@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // ================= producer: work queue + block table + TMA =================
         // (Measured alternatives -- control loads run ahead, lane-0-only tile loop,
         // block-table chunk prefetch -- were all slower on B200.)
+        const int n_items = p.hdr->n_items;    // this step's work-list length (device header)
         int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
 #pragma unroll
         for (int q = 0; q < NC; ++q) pc[q] = 0;
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             const int slot = k % IR, use = k / IR;
             if (lane == 0 && use > 0) mbar_wait(iempty0 + 8 * slot, (use - 1) & 1);
             __syncwarp();
-            if (idx >= p.n_items) {
+            if (idx >= n_items) {
                 if (lane == 0) {
                     ring[slot].it.nblk = 0;   // sentinel: no more items
                     mbar_arrive(ifull0 + 8 * slot);
@@ -650,7 +651,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 template <int DT, int G>
 __global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
-    merge_pair<DT, G>(p, p.merges[blockIdx.x], threadIdx.x, blockDim.x);
+    const int n = p.hdr->n_merges;                          // fixed grid, grid-stride over this step's pairs
+    for (int i = blockIdx.x; i < n; i += gridDim.x) merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x);
 }
 
 template <int DT, int G> cudaError_t prepare() {
@@ -688,10 +690,11 @@ cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStrea
                                          tm.v, p)
                             : launch_pdl(apex_decode_kernel<DT, G, false>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s,
                                          tm.k, tm.v, p);
-        if (e != cudaSuccess || p.fuse_merge || p.n_merges == 0) return e;
+        if (e != cudaSuccess || p.fuse_merge) return e;
     }
-    if (p.n_merges > 0) return launch_pdl(apex_merge_kernel<DT, G>, p.n_merges, 128, 0, s, p);
-    return cudaSuccess;
+    // launched whenever merges are not fused, even if this step has none (it then
+    // exits at once): the launch sequence never depends on the step's plan
+    return launch_pdl(apex_merge_kernel<DT, G>, p.merge_grid, 128, 0, s, p);
 }
 
 }  // namespace
