@@ -128,8 +128,10 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
    fp32).  Attends over seq_lens[seq] tokens, INCLUDING this step's appended
    token (reading c3).  scale is usually 1/sqrt(D) (reading c1).  Split-KV
    flash-decode (FlashDecoding lineage): one persistent kernel over the
-   planned work items + (if any (seq, kv-head) was split) one log-sum-exp
-   merge kernel.  Results are deterministic and independent of the physical
+   planned work items, plus one log-sum-exp merge kernel for the split
+   (seq, kv-head) pairs -- or, for small steps (latency regime), the merge is
+   done inside the decode kernel by the last split to finish (see
+   apex_kv_decode_launches).  Results are deterministic and independent of the physical
    block placement.  Supported: F32/F16 with g == 1 (CUDA cores), F16/BF16
    with g in {2,4,8} (tensor cores, mma.sync); otherwise APEX_EUNSUPPORTED. */
 apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out,
