@@ -235,3 +235,49 @@ def test_compute_sanitizer_small(cuda_lib, tool, tmp_path):
     assert r.returncode == 0 and "done" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
     summary = r.stdout + r.stderr
     assert "ERROR SUMMARY: 0 errors" in summary or "(0 errors, 0 warnings)" in summary, summary[-2000:]
+
+
+def test_continuous_batching_churn(cuda_lib):
+    """Serving-style churn: requests finish (apex_kv_release) and new ones arrive
+    and reuse freed blocks (which still hold stale K/V) while others keep
+    decoding; every step is checked against the oracle on the live batch."""
+    import torch
+    rng = np.random.default_rng(7)
+    hq, hkv, dtype = 16, 4, "bf16"
+    cache = make_cache(dtype, hq, hkv, num_blocks=600, max_seqs=32, max_blocks_per_seq=80, max_batch=32)
+    live = {}                                   # seq id -> current context length (tokens written)
+    next_b = 0
+    ids = {}                                    # seq id -> generator request id
+    for step in range(12):
+        # finish some, admit some
+        for s in list(live):
+            if rng.random() < 0.25:
+                cache.release(s)
+                del live[s]
+        free_ids = [s for s in range(32) if s not in live]
+        for s in free_ids[:int(rng.integers(1, 4))]:
+            n0 = int(rng.integers(1, 900))
+            ids[s] = next_b
+            next_b += 1
+            # prefill n0 - 1 tokens of the new request (generator keyed by its request id)
+            if n0 > 1:
+                cache.alloc([s], [n0 - 1])
+                k = gen_dev(cache, 1, 0, [ids[s]] * (n0 - 1), list(range(n0 - 1)), hkv)
+                v = gen_dev(cache, 2, 0, [ids[s]] * (n0 - 1), list(range(n0 - 1)), hkv)
+                cache.append(0, k, v)
+            live[s] = n0 - 1
+        seqs = sorted(live)
+        cache.alloc(seqs, [1] * len(seqs))
+        pos = [live[s] for s in seqs]
+        b_ids = [ids[s] for s in seqs]
+        k = gen_dev(cache, 1, 0, b_ids, pos, hkv)
+        v = gen_dev(cache, 2, 0, b_ids, pos, hkv)
+        cache.append(0, k, v)
+        q = gen_dev(cache, 0, 0, b_ids, pos, hq)
+        out = cache.decode(0, q)
+        torch.cuda.synchronize()
+        for s in seqs:
+            live[s] += 1
+        ctx = [live[s] for s in seqs]
+        ref = oracle_rows(b_ids, ctx, hq, hkv, dtype)
+        check_close(to_f64(out, dtype), ref, dtype)
