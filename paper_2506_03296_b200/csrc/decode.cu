@@ -44,6 +44,9 @@ namespace {
 #ifndef APEX_CTAS_PER_SM
 #define APEX_CTAS_PER_SM 2
 #endif
+#ifndef APEX_EARLY_RELEASE
+#define APEX_EARLY_RELEASE 0
+#endif
 #ifndef APEX_L2_EVICT_FIRST
 #define APEX_L2_EVICT_FIRST 0
 #endif
@@ -218,7 +221,9 @@ template <int DT, int G> struct MmaConsumer {
         l = 0.f;
     }
 
-    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float scale_log2, int lane) {
+    template <typename Release>
+    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float scale_log2, int lane,
+                                         Release release) {
         const int r8 = lane & 7, mi = lane >> 3, tid = lane & 3, row = lane >> 2;
         // ---- S = Q K^T  (16 x 16 tokens), k-steps over d
         float s[2][4];
@@ -233,6 +238,20 @@ template <int DT, int G> struct MmaConsumer {
             mma_16816<DT>(s[0], qa[kk][0], qa[kk][1], b0, b1);
             mma_16816<DT>(s[1], qa[kk][0], qa[kk][1], b2, b3);
         }
+#if APEX_EARLY_RELEASE
+        // V fragments to registers now, then hand the slot back before softmax + P.V
+        uint32_t vf[8][4];
+        {
+            const uint32_t v_lane0 = vt + (uint32_t)(((mi & 1) * 8 + r8) * 128);
+#pragma unroll
+            for (int nd = 0; nd < 16; nd += 2) {
+                const int c = (nd & 7) + (mi >> 1);
+                ldsm_x4_t(v_lane0 + (nd >> 3) * 2048 + ((c ^ r8) << 4), vf[nd / 2][0], vf[nd / 2][1],
+                          vf[nd / 2][2], vf[nd / 2][3]);
+            }
+        }
+        release();
+#endif
         // ---- online softmax over this tile's 16 tokens (row = lane/4)
         float x[4];
         x[0] = (tid * 2 < valid) ? s[0][0] * scale_log2 : -INFINITY;
@@ -262,6 +281,13 @@ template <int DT, int G> struct MmaConsumer {
             mlo = (tid * 2 < valid ? 0x0000ffffu : 0u) | (tid * 2 + 1 < valid ? 0xffff0000u : 0u);
             mhi = (8 + tid * 2 < valid ? 0x0000ffffu : 0u) | (8 + tid * 2 + 1 < valid ? 0xffff0000u : 0u);
         }
+#if APEX_EARLY_RELEASE
+#pragma unroll
+        for (int nd = 0; nd < 16; nd += 2) {
+            mma_16816<DT>(o[nd], a0, a2, vf[nd / 2][0] & mlo, vf[nd / 2][1] & mhi);
+            mma_16816<DT>(o[nd + 1], a0, a2, vf[nd / 2][2] & mlo, vf[nd / 2][3] & mhi);
+        }
+#else
         const uint32_t v_lane = vt + (uint32_t)(((mi & 1) * 8 + r8) * 128);
 #pragma unroll
         for (int nd = 0; nd < 16; nd += 2) {
@@ -271,6 +297,8 @@ template <int DT, int G> struct MmaConsumer {
             mma_16816<DT>(o[nd], a0, a2, b0 & mlo, b1 & mhi);
             mma_16816<DT>(o[nd + 1], a0, a2, b2 & mlo, b3 & mhi);
         }
+        release();
+#endif
     }
 
     __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
@@ -332,7 +360,8 @@ template <int DT> struct SimtConsumer {
         l = 0.f;
     }
 
-    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float, int lane) {
+    template <typename Release>
+    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float, int lane, Release release) {
         const int t = lane & 15, hh = lane >> 4, t7 = t & 7;
         // ---- s_t (log2 units): lane t, dims of half hh
         float acc = 0.f;
@@ -408,6 +437,7 @@ template <int DT> struct SimtConsumer {
                 }
             }
         }
+        release();
     }
 
     __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
@@ -593,9 +623,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 mbar_wait(full0 + 8 * s, u & 1);
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;
-                st.tile(kt, kt + TILE, valid, p.scale_log2, lane);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty0 + 8 * s);
+                st.tile(kt, kt + TILE, valid, p.scale_log2, lane, [&] {
+                    __syncwarp();                                 // every lane's smem reads of the slot are done
+                    if (lane == 0) mbar_arrive(empty0 + 8 * s);   // release it to the producer
+                });
             }
             st.finish(cb_o, cb_m, cb_l, wc, lane);
             named_bar_sync(1, NC * 32);
