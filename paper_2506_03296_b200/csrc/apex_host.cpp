@@ -590,7 +590,7 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
     p.part_ml = (float *)(ws + kv->ws.part_ml);
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
     p.merge_counters = (int32_t *)(ws + kv->ws.merge_counters);
-    p.merge_grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kv->ws.max_merges, 2LL * kv->sm_count));
+    p.merge_grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kv->ws.max_merges, 16LL * kv->sm_count));
     p.max_blocks_per_seq = kv->d.max_blocks_per_seq;
     p.num_q_heads = kv->d.num_q_heads;
     p.num_kv_heads = kv->d.num_kv_heads;

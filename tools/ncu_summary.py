@@ -96,7 +96,7 @@ def main():
         sp = os.path.join(prof, "ncu_summary.json")
         summ = json.load(open(sp)) if os.path.exists(sp) else {}
         summ[a.config] = {"decode_dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                          "duration_us": float(d["gpu__time_duration.sum"][0]), "tag": a.tag}
+                          "duration_us": float(d["gpu__time_duration.sum"][0]) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[d["gpu__time_duration.sum"][1]], "tag": a.tag}
         json.dump(summ, open(sp, "w"), indent=1)
     if a.bench:
         import shutil
