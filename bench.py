@@ -27,7 +27,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -45,7 +44,6 @@ from synth import TENSOR_K, TENSOR_Q, TENSOR_V, WORKLOADS  # noqa: E402
 
 METRIC = "decode-attention tokens/s and achieved HBM GB/s vs ~8 TB/s at 1/2/4/8 B200"
 UNIT = "tokens/s"
-L2_BYTES = 126 * 2 ** 20
 FALLBACK_HBM_GBS = 6650.0
 
 

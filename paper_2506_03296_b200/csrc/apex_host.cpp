@@ -216,7 +216,6 @@ struct apex_kv {
     std::vector<apex::TmaPair> tmaps;
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
     bool fuse_merge = false;
-    int64_t last_chunk = 0;
 };
 
 extern "C" {
@@ -390,11 +389,11 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
                                                : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
     std::vector<int32_t> nblks(B);
     int64_t T = 0;
-    int32_t max_nblk = 1;
+
     for (int32_t b = 0; b < B; ++b) {
         nblks[b] = (int32_t)cdiv(lens[b], kv->d.block_size);
         T += (int64_t)nblks[b] * Hkv;
-        max_nblk = std::max(max_nblk, nblks[b]);
+
     }
     int64_t chunk;
     bool latency = false;
@@ -406,7 +405,6 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     } else {
         chunk = std::max<int64_t>(4, cdiv(T, 16 * P));
     }
-    (void)max_nblk;
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;
     std::vector<int32_t> pc;
@@ -433,7 +431,6 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     kv->items.swap(items);
     kv->merges.swap(merges);
     kv->fuse_merge = latency;
-    kv->last_chunk = chunk;
     return APEX_OK;
 }
 

@@ -27,7 +27,7 @@
 //    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
 //    (m, l, unnormalised O) fp32 partials merged in split order -- by a second
-//    small launch (one CTA per split pair) in the bandwidth regime, or, in the
+//    small launch (fixed grid, grid-stride over split pairs) in the bandwidth regime, or, in the
 //    latency regime, by the last split of the pair to finish (per-pair arrival
 //    counter) inside this kernel, saving the launch.
 #include <cuda_bf16.h>

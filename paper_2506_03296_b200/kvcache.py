@@ -29,7 +29,7 @@ class PagedKVCache:
     def __init__(self, *, num_layers: int, num_q_heads: int, num_kv_heads: int, num_blocks: int,
                  max_seqs: int, max_blocks_per_seq: int, max_batch: int, max_new_tokens: int,
                  dtype: str = "bf16", head_dim: int = 128, block_size: int = 16, device="cuda",
-                 host_only: bool = False, alloc_pools: bool = True):
+                 host_only: bool = False):
         self.num_layers, self.num_q_heads, self.num_kv_heads = num_layers, num_q_heads, num_kv_heads
         self.head_dim, self.block_size, self.dtype = head_dim, block_size, dtype
         self.num_blocks, self.max_seqs, self.max_blocks_per_seq = num_blocks, max_seqs, max_blocks_per_seq
