@@ -50,13 +50,13 @@ def main():
         e.record(comp)
 
     def resident():
-        cache.alloc(seqs, [0] * B)
+        cache.alloc(seqs, [1] * B)
         for _ in range(L):
             cache.append(0, k, v)
             cache.decode(0, q, out=out)
 
     def serial():
-        cache.alloc(seqs, [0] * B)
+        cache.alloc(seqs, [1] * B)
         for _ in range(L):
             qd[0].copy_(qh, non_blocking=True)
             kd[0].copy_(kh, non_blocking=True)
@@ -66,7 +66,7 @@ def main():
             oh.copy_(od[0], non_blocking=True)
 
     def overlapped():
-        cache.alloc(seqs, [0] * B)
+        cache.alloc(seqs, [1] * B)
         for l in range(L):
             j = l % 2
             with torch.cuda.stream(copy):
