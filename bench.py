@@ -487,7 +487,10 @@ def run_apex(args):
         kd = [torch.empty_like(ks[0]) for _ in range(NB)]
         vd = [torch.empty_like(vs[0]) for _ in range(NB)]
         od = [torch.empty_like(qs[0]) for _ in range(NB)]
-        comp, copy = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+        # separate H2D and D2H streams: on one in-order copy stream the H2D of layer l+1
+        # would queue behind the D2H of layer l, i.e. behind layer l's decode (measured:
+        # no overlap at all, tools/e2e_probe.py)
+        comp, h2d_s, d2h_s = torch.cuda.current_stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         h2d_done = [torch.cuda.Event() for _ in range(NB)]
         dec_done = [torch.cuda.Event() for _ in range(NB)]
         buf_free = [torch.cuda.Event() for _ in range(NB)]
@@ -498,12 +501,12 @@ def run_apex(args):
             cache.alloc(seq, ones)
             for l in range(L):
                 p, j = l % P, l % NB
-                with torch.cuda.stream(copy):
-                    copy.wait_event(buf_free[j])
+                with torch.cuda.stream(h2d_s):
+                    h2d_s.wait_event(buf_free[j])
                     qd[j].copy_(qh[p], non_blocking=True)
                     kd[j].copy_(kh[p], non_blocking=True)
                     vd[j].copy_(vh[p], non_blocking=True)
-                    h2d_done[j].record(copy)
+                    h2d_done[j].record(h2d_s)
                 comp.wait_event(h2d_done[j])
                 cache.append(p, kd[j], vd[j])
                 cache.decode(p, qd[j], out=od[j])
@@ -512,10 +515,10 @@ def run_apex(args):
                     buf_free[j].record(comp)
                     continue
                 dec_done[j].record(comp)
-                with torch.cuda.stream(copy):
-                    copy.wait_event(dec_done[j])
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(dec_done[j])
                     oh[p].copy_(od[j], non_blocking=True)
-                    buf_free[j].record(copy)
+                    buf_free[j].record(d2h_s)
 
         for _ in range(W):
             e2e_step()
@@ -534,8 +537,8 @@ def run_apex(args):
         result["e2e"] = {"value": total_tokens / (e_ms * 1e-3), "unit": UNIT,
                          "h2d_bytes_per_step": L * B * (hq + 2 * hkv) * D * es,
                          "d2h_bytes_per_step": L * B * hq * D * es, "ms_per_step": e_ms / K,
-                         "path": "pinned host q/k/v -> H2D on a copy stream (double-buffered, overlapped with the "
-                                 "previous layer) -> PagedKVCache.append/decode (C ABI) -> D2H of out on the copy "
+                         "path": "pinned host q/k/v -> H2D on an H2D stream (double-buffered, overlapped with the "
+                                 "previous layer) -> PagedKVCache.append/decode (C ABI) -> D2H of out on a D2H "
                                  "stream -> pinned host"}
     if rank == 0:
         line = json.dumps(result)

@@ -42,7 +42,7 @@ def main():
     kd = [torch.empty_like(k) for _ in range(2)]
     vd = [torch.empty_like(v) for _ in range(2)]
     od = [torch.empty_like(out) for _ in range(2)]
-    comp, copy = torch.cuda.current_stream(), torch.cuda.Stream()
+    comp, copy, d2h_s = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
     h2d = [torch.cuda.Event() for _ in range(2)]
     dec = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]
@@ -79,10 +79,10 @@ def main():
             cache.append(0, kd[j], vd[j])
             cache.decode(0, qd[j], out=od[j])
             dec[j].record(comp)
-            with torch.cuda.stream(copy):
-                copy.wait_event(dec[j])
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(dec[j])
                 oh.copy_(od[j], non_blocking=True)
-                free[j].record(copy)
+                free[j].record(d2h_s)
         for e in free:
             comp.wait_event(e)
 
