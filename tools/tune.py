@@ -32,7 +32,8 @@ def main():
     w = WORKLOADS[a.config]
     ctx = [int(c) for c in w.contexts()]
     B = len(ctx)
-    cache = make_cache(w.dtype, w.num_q_heads, w.num_kv_heads, sum(-(-(c + 1) // 16) for c in ctx) + 16,
+    mult = int(os.environ.get("APEX_TUNE_BLOCK_MULT", "1"))     # >1: spare pool rows for layout experiments
+    cache = make_cache(w.dtype, w.num_q_heads, w.num_kv_heads, mult * (sum(-(-(c + 1) // 16) for c in ctx) + 16),
                        max_seqs=B, max_blocks_per_seq=-(-(max(ctx) + 1) // 16) + 1, max_new_tokens=1 << 22)
     seqs = list(range(B))
     prefill(cache, seqs, ctx)
