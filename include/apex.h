@@ -31,7 +31,7 @@
  *     so the per-layer calls may be captured once and replayed every step with
  *     apex_kv_alloc called outside the graph before each replay.  q/out/k_new/
  *     v_new must then be the same (static) buffers at every replay.
- *   - Host-only handles (desc.k_pool == NULL and desc.block_table == NULL) run
+ *   - Host-only handles (desc.kv_pool == NULL and desc.block_table == NULL) run
  *     the allocator and planner without any CUDA call; append/decode then
  *     return APEX_EINVAL.  Used by CPU tests and host-side planning.
  */
@@ -61,7 +61,7 @@ typedef struct apex_cost apex_cost;
 typedef void *apex_stream;   /* cudaStream_t */
 
 typedef struct {
-    int32_t num_layers;          /* physical layers that own a pool pair (1..64) */
+    int32_t num_layers;          /* physical layers that own a KV pool (1..64) */
     int32_t num_q_heads;         /* Hq (local to this rank when heads are sharded) */
     int32_t num_kv_heads;        /* Hkv; Hq % Hkv == 0, group g = Hq/Hkv in {1,2,4,8} */
     int32_t head_dim;            /* D; must be 128 */
@@ -72,11 +72,13 @@ typedef struct {
     int32_t max_batch;           /* max sequences in one apex_kv_alloc call (decode batch) */
     int32_t max_new_tokens;      /* max sum(n_new) in one apex_kv_alloc call */
     apex_dtype dtype;
-    /* [num_layers] device pointers; each pool is [num_blocks][Hkv][block_size][D]
-       elements of `dtype`, 128-byte aligned.  Pools may alias (logical layers
-       mapped onto fewer physical layers is the caller's choice). */
-    void *const *k_pool;
-    void *const *v_pool;
+    /* [num_layers] device pointers, one KV pool per physical layer, each
+       [num_blocks][Hkv][2][block_size][D] elements of `dtype` (index 0 = K,
+       1 = V), 128-byte aligned: the K and V rows of one (block, kv head) are
+       one contiguous 2*16*D-element tile, fetched by a single TMA.  Pools may
+       alias (logical layers mapped onto fewer physical layers is the caller's
+       choice). */
+    void *const *kv_pool;
     int32_t *block_table;        /* device int32 [max_seqs][max_blocks_per_seq] */
     int32_t *seq_lens;           /* device int32 [max_seqs] */
     void *workspace;             /* device scratch, >= apex_kv_workspace_bytes(desc), 256-B aligned */
@@ -89,7 +91,7 @@ size_t apex_kv_workspace_bytes(const apex_kv_desc *desc);
 
 /* Validate the desc, build the LIFO free list (first pop = block 0, reading
    c10), the host mirrors, the pinned staging ring and one TMA descriptor per
-   (physical layer, K/V).  Launches no kernel.  The pools' contents are not
+   physical layer.  Launches no kernel.  The pools' contents are not
    touched (callers may pre-fill them, e.g. with NaN in tests). */
 apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out);
 
@@ -117,8 +119,9 @@ apex_status apex_kv_release(apex_kv *kv, int32_t seq_id);
 /* Write this step's new K and V vectors of physical layer `layer` into the
    pools (one K and one V vector per token per layer).  k_new, v_new:
    device [sum(n_new)][Hkv][D] of dtype, rows ordered as defined by the last
-   apex_kv_alloc.  Bit-exact copy: K_pool[layer][blk][h][t][:] = k_new[row][h][:]
-   with (blk, t) from the row's slot.  One kernel launch. */
+   apex_kv_alloc.  Bit-exact copy: kv_pool[layer][blk][h][0][t][:] = k_new[row][h][:]
+   and kv_pool[layer][blk][h][1][t][:] = v_new[row][h][:], with (blk, t) from the
+   row's slot.  One kernel launch. */
 apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const void *v_new,
                            apex_stream stream);
 

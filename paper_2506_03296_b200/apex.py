@@ -40,7 +40,7 @@ class apex_kv_desc(ctypes.Structure):
     _fields_ = [("num_layers", c_int32), ("num_q_heads", c_int32), ("num_kv_heads", c_int32),
                 ("head_dim", c_int32), ("block_size", c_int32), ("num_blocks", c_int32), ("max_seqs", c_int32),
                 ("max_blocks_per_seq", c_int32), ("max_batch", c_int32), ("max_new_tokens", c_int32),
-                ("dtype", c_int), ("k_pool", POINTER(c_void_p)), ("v_pool", POINTER(c_void_p)),
+                ("dtype", c_int), ("kv_pool", POINTER(c_void_p)),
                 ("block_table", c_void_p), ("seq_lens", c_void_p), ("workspace", c_void_p),
                 ("workspace_bytes", c_size_t)]
 

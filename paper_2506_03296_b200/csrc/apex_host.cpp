@@ -48,7 +48,7 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int elem_bytes(apex_dtype dt) { return dt == APEX_F32 ? 4 : 2; }
 
-bool desc_host_only(const apex_kv_desc *d) { return d->k_pool == nullptr && d->block_table == nullptr; }
+bool desc_host_only(const apex_kv_desc *d) { return d->kv_pool == nullptr && d->block_table == nullptr; }
 
 int query_sm_count(bool host_only) {
     if (host_only) return 148;
@@ -117,15 +117,15 @@ apex_status validate_desc(const apex_kv_desc *d, bool need_workspace = true) {
         return fail(APEX_EINVAL, "num_blocks/max_seqs/max_blocks_per_seq/max_batch/max_new_tokens must be >= 1");
     if ((int64_t)d->max_blocks_per_seq * d->block_size > (1LL << 30))
         return fail(APEX_EINVAL, "max context too large");
-    if ((int64_t)d->num_blocks * d->num_kv_heads * d->block_size >= (1LL << 31))
+    if ((int64_t)d->num_blocks * d->num_kv_heads * 2 * d->block_size >= (1LL << 31))
         return fail(APEX_EUNSUPPORTED, "pool rows exceed the TMA coordinate range");
     if (d->max_batch > d->max_seqs) return fail(APEX_EINVAL, "max_batch > max_seqs");
     if (!desc_host_only(d)) {
-        if (!d->k_pool || !d->v_pool || !d->block_table || !d->seq_lens || (need_workspace && !d->workspace))
-            return fail(APEX_EINVAL, "device desc needs k_pool, v_pool, block_table, seq_lens, workspace");
+        if (!d->kv_pool || !d->block_table || !d->seq_lens || (need_workspace && !d->workspace))
+            return fail(APEX_EINVAL, "device desc needs kv_pool, block_table, seq_lens, workspace");
         for (int l = 0; l < d->num_layers; ++l) {
-            if (!d->k_pool[l] || !d->v_pool[l]) return fail(APEX_EINVAL, "pool pointer of layer %d is NULL", l);
-            if (((uintptr_t)d->k_pool[l] | (uintptr_t)d->v_pool[l]) & 127)
+            if (!d->kv_pool[l]) return fail(APEX_EINVAL, "pool pointer of layer %d is NULL", l);
+            if ((uintptr_t)d->kv_pool[l] & 127)
                 return fail(APEX_EINVAL, "pools of layer %d are not 128-byte aligned", l);
         }
         if (need_workspace && ((uintptr_t)d->workspace & 255)) return fail(APEX_EINVAL, "workspace not 256-byte aligned");
@@ -147,11 +147,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// TMA view of one pool: rows = (block*Hkv + head)*16 + t, each row D elements.
-// Preferred 3-D view {128-B segment elements, rows, segments} with 128-B
-// swizzle loads a whole (block, head) tile with ONE cp.async.bulk.tensor into
-// smem laid out [segment][16 rows][128 B]; the 2-D fallback issues one op per
-// segment into the same layout.
+// TMA view of one pool: rows = ((block*Hkv + head)*2 + {K,V})*16 + t, each row D
+// elements.  Preferred 3-D view {128-B segment elements, rows, segments} with
+// 128-B swizzle loads a whole (block, head) K+V tile (32 rows) with ONE
+// cp.async.bulk.tensor into smem laid out [segment][32 rows][128 B] (K rows
+// 0-15, V rows 16-31); the 2-D fallback issues one op per segment into the same
+// layout.
 bool encode_pool(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap *m, void *base, apex_dtype dt,
                  int64_t rows, int segs_mode) {
     const int es = elem_bytes(dt);
@@ -165,14 +166,14 @@ bool encode_pool(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap *m, void *ba
     if (segs_mode == 1) {
         cuuint64_t dims[3] = {seg_elems, (cuuint64_t)rows, segs};
         cuuint64_t strides[2] = {row_bytes, 128};
-        cuuint32_t box[3] = {seg_elems, (cuuint32_t)apex::kBlock, segs};
+        cuuint32_t box[3] = {seg_elems, (cuuint32_t)(2 * apex::kBlock), segs};   // K and V rows of a tile
         r = enc(m, tdt, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         cuuint64_t dims[2] = {(cuuint64_t)apex::kHeadDim, (cuuint64_t)rows};
         cuuint64_t strides[1] = {row_bytes};
-        cuuint32_t box[2] = {seg_elems, (cuuint32_t)apex::kBlock};
+        cuuint32_t box[2] = {seg_elems, (cuuint32_t)(2 * apex::kBlock)};
         r = enc(m, tdt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -184,7 +185,7 @@ bool encode_pool(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap *m, void *ba
 
 struct apex_kv {
     apex_kv_desc d{};
-    std::vector<void *> k_pools, v_pools;
+    std::vector<void *> kv_pools;
     bool host_only = true;
     int sm_count = 148;
     int group = 1;
@@ -213,7 +214,7 @@ struct apex_kv {
     bool staged_pending[2] = {false, false};
     int ring = 0;
 
-    std::vector<apex::TmaPair> tmaps;
+    std::vector<apex::TmaMap> tmaps;
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
     bool fuse_merge = false;
 };
@@ -249,10 +250,8 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
             return fail(APEX_EINVAL, "workspace_bytes %zu < required %zu", desc->workspace_bytes,
                         (size_t)apex_kv_workspace_bytes(desc));
         }
-        kv->k_pools.assign(desc->k_pool, desc->k_pool + desc->num_layers);
-        kv->v_pools.assign(desc->v_pool, desc->v_pool + desc->num_layers);
-        kv->d.k_pool = kv->k_pools.data();
-        kv->d.v_pool = kv->v_pools.data();
+        kv->kv_pools.assign(desc->kv_pool, desc->kv_pool + desc->num_layers);
+        kv->d.kv_pool = kv->kv_pools.data();
         for (int i = 0; i < 2; ++i) {
             cudaError_t e = cudaHostAlloc((void **)&kv->staging[i], kv->ws.upload_cap, cudaHostAllocDefault);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->staged[i], cudaEventDisableTiming);
@@ -266,13 +265,13 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
             apex_kv_destroy(kv);
             return fail(APEX_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
         }
-        const int64_t rows = (int64_t)desc->num_blocks * desc->num_kv_heads * desc->block_size;
+        // pool rows: ((block * Hkv + head) * 2 + {K, V}) * 16 + t
+        const int64_t rows = (int64_t)desc->num_blocks * desc->num_kv_heads * 2 * desc->block_size;
         kv->tmaps.resize(desc->num_layers);
         for (int mode : {1, 2}) {
             bool ok = true;
             for (int l = 0; l < desc->num_layers && ok; ++l)
-                ok = encode_pool(enc, &kv->tmaps[l].k, kv->k_pools[l], desc->dtype, rows, mode) &&
-                     encode_pool(enc, &kv->tmaps[l].v, kv->v_pools[l], desc->dtype, rows, mode);
+                ok = encode_pool(enc, &kv->tmaps[l].kv, kv->kv_pools[l], desc->dtype, rows, mode);
             if (ok) {
                 kv->tma_segs = mode == 1 ? 1 : apex::kHeadDim * elem_bytes(desc->dtype) / 128;
                 break;
@@ -559,7 +558,7 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
     if (((uintptr_t)k_new | (uintptr_t)v_new) & 15) return fail(APEX_EINVAL, "k_new/v_new not 16-byte aligned");
     // always one launch (it reads the row count from the step header): graph-capturable
     uint8_t *up = (uint8_t *)kv->d.workspace + kv->ws.upload;
-    cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->k_pools[layer], kv->v_pools[layer],
+    cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->kv_pools[layer],
                                         (const int32_t *)(up + kv->ws.o_tail), (const apex::StepHeader *)up,
                                         kv->d.num_kv_heads, kv->sm_count, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_kv_append");

@@ -65,18 +65,17 @@ struct DecodeParams {
     int32_t fuse_merge;        // 1: last split per pair merges in-kernel; 0: apex_merge_kernel launch
 };
 
-struct TmaPair {
-    CUtensorMap k;             // 64-byte aligned opaque descriptors
-    CUtensorMap v;
+struct TmaMap {
+    CUtensorMap kv;            // 64-byte aligned opaque descriptor of one layer's KV pool
 };
 
 // launchers: return cudaSuccess or the launch error
 cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
                                 int32_t *block_table, int32_t *seq_lens, cudaStream_t s);
-cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool,
-                          void *v_pool, const int32_t *slots, const StepHeader *hdr, int n_kv_heads,
-                          int sm_count, cudaStream_t s);
-cudaError_t launch_decode(apex_dtype dt, int group, const TmaPair &tm, const DecodeParams &p,
+cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *kv_pool,
+                          const int32_t *slots, const StepHeader *hdr, int n_kv_heads, int sm_count,
+                          cudaStream_t s);
+cudaError_t launch_decode(apex_dtype dt, int group, const TmaMap &tm, const DecodeParams &p,
                           int grid, cudaStream_t s);
 // persistent-grid size the decode kernel of (dtype, group) runs with on this device
 int decode_grid_ctas(apex_dtype dt, int group, int sm_count);

@@ -2,17 +2,16 @@
 // per-step block-table / length delta application (P:156 dynamic KV management).
 //
 // append: one thread per 16-byte chunk of a (row, head) vector; 128-bit loads
-// and stores.  Pool layout [num_blocks][Hkv][16][D]: a (block, head) tile is
-// contiguous, so the 16 tokens of a block share a 4 KiB (16-bit) / 8 KiB (fp32)
-// tile that the decode kernel fetches with one TMA.  Pure bit copy.
+// and stores.  Pool layout [num_blocks][Hkv][2][16][D]: the K rows and then the
+// V rows of one (block, head) form one contiguous 8 KiB (16-bit) / 16 KiB (fp32)
+// tile that the decode kernel fetches with a single TMA.  Pure bit copy.
 #include "apex_internal.h"
 
 namespace apex {
 namespace {
 
 __global__ void __launch_bounds__(256) apex_append_kernel(const uint4 *__restrict__ k_new,
-                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_pool,
-                                                          uint4 *__restrict__ v_pool,
+                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ kv_pool,
                                                           const int32_t *__restrict__ slots,
                                                           const StepHeader *__restrict__ hdr, int hkv,
                                                           int chunks_per_vec) {
@@ -28,11 +27,8 @@ __global__ void __launch_bounds__(256) apex_append_kernel(const uint4 *__restric
         const int64_t row = rh / hkv;
         const int32_t slot = __ldg(slots + row);
         const int64_t blk = slot / kBlock, t = slot % kBlock;
-        const int64_t dst = ((blk * hkv + h) * kBlock + t) * chunks_per_vec + c;
-        if (is_v)
-            v_pool[dst] = __ldg(v_new + j);
-        else
-            k_pool[dst] = __ldg(k_new + j);
+        const int64_t dst = (((blk * hkv + h) * 2 + (is_v ? 1 : 0)) * kBlock + t) * chunks_per_vec + c;
+        kv_pool[dst] = __ldg((is_v ? v_new : k_new) + j);
     }
 }
 
@@ -62,14 +58,14 @@ cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_
 }
 
 // Fixed grid (grid-stride over hdr->n_rows) so the launch is step-invariant.
-cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *kv_pool,
                           const int32_t *slots, const StepHeader *hdr, int n_kv_heads, int sm_count,
                           cudaStream_t s) {
     const int es = dt == APEX_F32 ? 4 : 2;
     const int cpv = kHeadDim * es / 16;
     apex_append_kernel<<<sm_count * 8, 256, 0, s>>>(static_cast<const uint4 *>(k_new),
-                                                    static_cast<const uint4 *>(v_new), static_cast<uint4 *>(k_pool),
-                                                    static_cast<uint4 *>(v_pool), slots, hdr, n_kv_heads, cpv);
+                                                    static_cast<const uint4 *>(v_new), static_cast<uint4 *>(kv_pool),
+                                                    slots, hdr, n_kv_heads, cpv);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,9 @@ constexpr int NTHREADS = 32 * (NC + 1);
 constexpr int IR = 4;                    // item-ring entries
 constexpr int CTAS_PER_SM = APEX_CTAS_PER_SM;
 constexpr int kTileRows = kBlock;        // 16 tokens per tile
+// smem tile of one (block, kv head): [segment][32 rows: K 0-15, V 16-31][128 B], 128-B swizzled
+constexpr int kSegStride = 2 * kTileRows * 128;
+constexpr int kVOff = kTileRows * 128;
 
 struct ItemSlot {
     WorkItem it;
@@ -65,7 +68,7 @@ constexpr int kSmemPerCta = (232448 - 1024 * CTAS_PER_SM) / CTAS_PER_SM - 1024; 
 
 template <int DT, int G> struct Cfg {
     static constexpr int ES = DT == APEX_F32 ? 4 : 2;
-    static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of one K (or V) tile
+    static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of the K (or the V) half of a tile
     static constexpr int CB_O = NC * G * kHeadDim * 4;       // per-warp O for the item merge
     static constexpr int CB_ML = NC * G * 2 * 4 + 16;     // + merge flag
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
@@ -234,7 +237,7 @@ template <int DT, int G> struct MmaConsumer {
         for (int kk = 0; kk < 8; ++kk) {
             const int c = (kk & 3) * 2 + (mi & 1);
             uint32_t b0, b1, b2, b3;
-            ldsm_x4(k_lane + (kk >> 2) * 2048 + ((c ^ r8) << 4), b0, b1, b2, b3);
+            ldsm_x4(k_lane + (kk >> 2) * kSegStride + ((c ^ r8) << 4), b0, b1, b2, b3);
             mma_16816<DT>(s[0], qa[kk][0], qa[kk][1], b0, b1);
             mma_16816<DT>(s[1], qa[kk][0], qa[kk][1], b2, b3);
         }
@@ -246,7 +249,7 @@ template <int DT, int G> struct MmaConsumer {
 #pragma unroll
             for (int nd = 0; nd < 16; nd += 2) {
                 const int c = (nd & 7) + (mi >> 1);
-                ldsm_x4_t(v_lane0 + (nd >> 3) * 2048 + ((c ^ r8) << 4), vf[nd / 2][0], vf[nd / 2][1],
+                ldsm_x4_t(v_lane0 + (nd >> 3) * kSegStride + ((c ^ r8) << 4), vf[nd / 2][0], vf[nd / 2][1],
                           vf[nd / 2][2], vf[nd / 2][3]);
             }
         }
@@ -293,7 +296,7 @@ template <int DT, int G> struct MmaConsumer {
         for (int nd = 0; nd < 16; nd += 2) {
             const int c = (nd & 7) + (mi >> 1);
             uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(v_lane + (nd >> 3) * 2048 + ((c ^ r8) << 4), b0, b1, b2, b3);
+            ldsm_x4_t(v_lane + (nd >> 3) * kSegStride + ((c ^ r8) << 4), b0, b1, b2, b3);
             mma_16816<DT>(o[nd], a0, a2, b0 & mlo, b1 & mhi);
             mma_16816<DT>(o[nd + 1], a0, a2, b2 & mlo, b3 & mhi);
         }
@@ -368,7 +371,7 @@ template <int DT> struct SimtConsumer {
         if constexpr (F32) {
 #pragma unroll
             for (int sg = 0; sg < 2; ++sg) {
-                const uint32_t rowa = kt + (uint32_t)((2 * hh + sg) * 2048 + t * 128);
+                const uint32_t rowa = kt + (uint32_t)((2 * hh + sg) * kSegStride + t * 128);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint4 k4 = lds128(rowa + ((c ^ t7) << 4));
@@ -380,7 +383,7 @@ template <int DT> struct SimtConsumer {
                 }
             }
         } else {
-            const uint32_t rowa = kt + (uint32_t)(hh * 2048 + t * 128);
+            const uint32_t rowa = kt + (uint32_t)(hh * kSegStride + t * 128);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint4 k4 = lds128(rowa + ((c ^ t7) << 4));
@@ -412,7 +415,7 @@ template <int DT> struct SimtConsumer {
             for (int r = 0; r < kTileRows; ++r) {
                 const float pr = __shfl_sync(0xffffffffu, pt, r);
                 if (r < valid) {
-                    uint4 v4 = lds128(vt + (uint32_t)(sg * 2048 + r * 128) + ((c ^ (r & 7)) << 4));
+                    uint4 v4 = lds128(vt + (uint32_t)(sg * kSegStride + r * 128) + ((c ^ (r & 7)) << 4));
                     o[0] = fmaf(pr, __uint_as_float(v4.x), o[0]);
                     o[1] = fmaf(pr, __uint_as_float(v4.y), o[1]);
                     o[2] = fmaf(pr, __uint_as_float(v4.z), o[2]);
@@ -426,7 +429,7 @@ template <int DT> struct SimtConsumer {
                 const int r = 2 * i + hh;
                 const float pr = __shfl_sync(0xffffffffu, pt, r);
                 if (r < valid) {
-                    uint4 v4 = lds128(vt + (uint32_t)(sg * 2048 + r * 128) + ((c ^ (r & 7)) << 4));
+                    uint4 v4 = lds128(vt + (uint32_t)(sg * kSegStride + r * 128) + ((c ^ (r & 7)) << 4));
                     const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -496,7 +499,7 @@ __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeIte
 // ------------------------------------------------------------------ decode kernel
 template <int DT, int G, bool FUSE>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
-    apex_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+    apex_decode_kernel(const __grid_constant__ CUtensorMap tmkv,
                        const DecodeParams p) {
     using C = Cfg<DT, G>;
     using S = C;
@@ -524,8 +527,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             mbar_init(iempty0 + 8 * i, NC);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmkv)) : "memory");
     }
     __syncthreads();
     // PDL: everything above overlapped the previous kernel; from here on we read
@@ -581,15 +583,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                         if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
                         const uint32_t bar = full0 + 8 * s;
                         mbar_expect_tx(bar, 2 * TILE);
-                        const int row = (phys * p.num_kv_heads + it.g) * kTileRows;
-                        const uint32_t dk = tiles_u + s * 2 * TILE, dv = dk + TILE;
+                        const int row = (phys * p.num_kv_heads + it.g) * 2 * kTileRows;   // K row 0 of the tile
+                        const uint32_t dk = tiles_u + s * 2 * TILE;
                         if (p.tma_segs == 1) {
-                            tma_load_3d(dk, &tmk, bar, 0, row, 0);
-                            tma_load_3d(dv, &tmv, bar, 0, row, 0);
+                            tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
                         } else {
                             for (int sg = 0; sg < p.tma_segs; ++sg) {
-                                tma_load_2d(dk + sg * 2048, &tmk, bar, sg * (128 / C::ES), row);
-                                tma_load_2d(dv + sg * 2048, &tmv, bar, sg * (128 / C::ES), row);
+                                tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
                             }
                         }
                     }
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 mbar_wait(full0 + 8 * s, u & 1);
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;
-                st.tile(kt, kt + TILE, valid, p.scale_log2, lane, [&] {
+                st.tile(kt, kt + kVOff, valid, p.scale_log2, lane, [&] {
                     __syncwarp();                                 // every lane's smem reads of the slot are done
                     if (lane == 0) mbar_arrive(empty0 + 8 * s);   // release it to the producer
                 });
@@ -714,13 +714,13 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, 
 }
 
 template <int DT, int G>
-cudaError_t launch(const TmaPair &tm, const DecodeParams &p, int grid, cudaStream_t s) {
+cudaError_t launch(const TmaMap &tm, const DecodeParams &p, int grid, cudaStream_t s) {
     if (grid > 0) {
         cudaError_t e = p.fuse_merge
-                            ? launch_pdl(apex_decode_kernel<DT, G, true>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.k,
-                                         tm.v, p)
+                            ? launch_pdl(apex_decode_kernel<DT, G, true>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.kv,
+                                         p)
                             : launch_pdl(apex_decode_kernel<DT, G, false>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s,
-                                         tm.k, tm.v, p);
+                                         tm.kv, p);
         if (e != cudaSuccess || p.fuse_merge) return e;
     }
     // launched whenever merges are not fused, even if this step has none (it then
@@ -757,7 +757,7 @@ cudaError_t decode_prepare(apex_dtype dt, int group) {
     }
 }
 
-cudaError_t launch_decode(apex_dtype dt, int group, const TmaPair &tm, const DecodeParams &p, int grid,
+cudaError_t launch_decode(apex_dtype dt, int group, const TmaMap &tm, const DecodeParams &p, int grid,
                           cudaStream_t s) {
     if (!decode_supported(dt, group)) return cudaErrorInvalidValue;
 #define APEX_LAUNCH_ARGS (tm, p, grid, s)

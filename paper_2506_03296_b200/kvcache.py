@@ -48,14 +48,14 @@ class PagedKVCache:
         if self.device.type == "cuda" and self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
         tdt = torch_dtype(dtype)
-        shape = (num_blocks, num_kv_heads, block_size, head_dim)
-        self.k_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
-        self.v_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
+        # one pool per physical layer: [num_blocks][Hkv][2 (K, V)][block_size][D]
+        shape = (num_blocks, num_kv_heads, 2, block_size, head_dim)
+        self.kv_pools = [torch.empty(shape, dtype=tdt, device=self.device) for _ in range(num_layers)]
+        self.k_pools = [t[:, :, 0] for t in self.kv_pools]      # views [num_blocks][Hkv][16][D]
+        self.v_pools = [t[:, :, 1] for t in self.kv_pools]
         self.block_table = torch.zeros((max_seqs, max_blocks_per_seq), dtype=torch.int32, device=self.device)
         self.seq_lens = torch.zeros((max_seqs,), dtype=torch.int32, device=self.device)
-        kp = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.k_pools])
-        vp = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.v_pools])
-        desc.k_pool, desc.v_pool = kp, vp
+        desc.kv_pool = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.kv_pools])
         desc.block_table, desc.seq_lens = self.block_table.data_ptr(), self.seq_lens.data_ptr()
         nbytes = A.apex_kv_workspace_bytes(desc)
         if nbytes == 0:

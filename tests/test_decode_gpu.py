@@ -23,7 +23,7 @@ def run_case(dtype, hq, hkv, ctx, qamp=1.0, split=None, interleave=0, seed=0, nu
     nb = num_blocks or sum(-(-c // 16) for c in ctx) + 8
     cache = make_cache(dtype, hq, hkv, nb, max_seqs=B + 4, max_blocks_per_seq=mbps)
     if poison:
-        for t in cache.k_pools + cache.v_pools:
+        for t in cache.kv_pools:
             t.view(torch.uint8).fill_(0xFF)        # NaN bit patterns in every dtype
     if split is not None:
         cache.set_split(split)
