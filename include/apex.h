@@ -140,6 +140,18 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
 apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out,
                                   float scale, apex_stream stream);
 
+/* As apex_decode_attention, but every output row is written to each of the
+   n_out (1..8) destinations outs[i] at element offset
+   b*out_row_stride + (out_head_offset + h)*D, h = this handle's q head.
+   With head sharding, rank r passes the symmetric (peer-mapped, e.g. over
+   NVLink) output buffers of all ranks and out_head_offset = r*Hq_local, so the
+   all-gather of head-sharded outputs happens inside the epilogue (SURVEY.md
+   §8(f) f3).  out_row_stride is in elements, a multiple of 4 and
+   >= (out_head_offset + Hq)*D; destinations 16-byte aligned. */
+apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
+                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
+                                     apex_stream stream);
+
 /* ---- planner knobs and introspection (host state only; no CUDA calls) ---- */
 
 /* Split-KV chunk in tokens (multiple of 16) used by the NEXT apex_kv_alloc;

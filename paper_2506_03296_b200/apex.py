@@ -25,7 +25,7 @@ EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex
            "apex_kv_append", "apex_decode_attention", "apex_kv_set_split", "apex_kv_set_grid",
            "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan",
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
-           "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches"]
+           "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex"]
 STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
 
 
@@ -92,6 +92,8 @@ def lib():
             "apex_pipelining_threshold": (c_int, [c_double, c_double, POINTER(c_double)]),
             "apex_decide": (c_int, [POINTER(apex_sched_input), POINTER(apex_decision)]),
             "apex_kv_decode_launches": (c_int32, [c_void_p]),
+            "apex_decode_attention_ex": (c_int, [c_void_p, c_int32, c_void_p, POINTER(c_void_p), c_int32, c_int64,
+                                                 c_int32, c_float, c_void_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -236,3 +238,10 @@ def apex_decide(n_prefill: int, n_gpu_decode: int, n_cpu_decode: int, n_g: float
 
 def apex_kv_decode_launches(kv: int) -> int:
     return int(lib().apex_kv_decode_launches(kv))
+
+
+def apex_decode_attention_ex(kv: int, layer: int, q_ptr: int, out_ptrs, out_row_stride: int, out_head_offset: int,
+                             scale: float, stream: int = 0) -> None:
+    outs = (c_void_p * max(len(out_ptrs), 1))(*[int(x) for x in out_ptrs])
+    _check(lib().apex_decode_attention_ex(kv, int(layer), q_ptr, outs, len(out_ptrs), int(out_row_stride),
+                                          int(out_head_offset), float(scale), stream))

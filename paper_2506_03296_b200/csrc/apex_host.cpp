@@ -567,15 +567,34 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
 apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out, float scale,
                                   apex_stream stream) {
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    void *outs[1] = {out};
+    return apex_decode_attention_ex(kv, layer, q, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim, 0, scale,
+                                    stream);
+}
+
+apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
+                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
+                                     apex_stream stream) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
     if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
     if (!kv->have_step) return fail(APEX_EINVAL, "apex_decode_attention before apex_kv_alloc");
     if (layer < 0 || layer >= kv->d.num_layers) return fail(APEX_EINVAL, "layer %d out of range", layer);
-    if (!q || !out) return fail(APEX_EINVAL, "q/out is NULL");
-    if (((uintptr_t)q | (uintptr_t)out) & 15) return fail(APEX_EINVAL, "q/out not 16-byte aligned");
+    if (!q || !outs || n_out < 1 || n_out > apex::kMaxOut)
+        return fail(APEX_EINVAL, "q/outs is NULL or n_out %d not in [1, %d]", n_out, apex::kMaxOut);
+    if (out_head_offset < 0 || out_row_stride % 4 ||
+        out_row_stride < (int64_t)(out_head_offset + kv->d.num_q_heads) * kv->d.head_dim)
+        return fail(APEX_EINVAL, "out_row_stride %lld / out_head_offset %d do not fit %d heads",
+                    (long long)out_row_stride, out_head_offset, kv->d.num_q_heads);
+    if ((uintptr_t)q & 15) return fail(APEX_EINVAL, "q not 16-byte aligned");
+    for (int32_t i = 0; i < n_out; ++i)
+        if (!outs[i] || ((uintptr_t)outs[i] & 15)) return fail(APEX_EINVAL, "outs[%d] NULL or not 16-byte aligned", i);
     if (!(scale > 0.0f) || !std::isfinite(scale)) return fail(APEX_EINVAL, "scale must be finite and > 0");
     apex::DecodeParams p{};
     p.q = q;
-    p.out = out;
+    for (int32_t i = 0; i < n_out; ++i) p.out[i] = outs[i];
+    p.n_out = n_out;
+    p.out_row_stride = out_row_stride;
+    p.out_head_offset = out_head_offset;
     p.block_table = kv->d.block_table;
     uint8_t *ws = (uint8_t *)kv->d.workspace;
     uint8_t *up = ws + kv->ws.upload;

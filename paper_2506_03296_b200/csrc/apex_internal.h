@@ -13,6 +13,7 @@ namespace apex {
 constexpr int kBlock = 16;          // tokens per KV block (reading c9)
 constexpr int kHeadDim = 128;       // D
 constexpr int kMaxLayers = 64;
+constexpr int kMaxOut = 8;          // destinations of apex_decode_attention_ex
 
 // One split-KV work item: the tokens of logical blocks [blk0, blk0+nblk) of
 // (batch row b, kv head g).  32 bytes, read once per item by the decode kernel.
@@ -47,7 +48,10 @@ struct __align__(16) StepHeader {
 
 struct DecodeParams {
     const void *q;             // [B][Hq][D]
-    void *out;                 // [B][Hq][D]
+    void *out[8];              // n_out destinations (local and/or peer-mapped), each written identically
+    int64_t out_row_stride;    // elements between consecutive batch rows of a destination
+    int32_t out_head_offset;   // head index of this handle's q-head 0 inside a destination row
+    int32_t n_out;
     const int32_t *block_table;
     const WorkItem *items;
     const MergeItem *merges;

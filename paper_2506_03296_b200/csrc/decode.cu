@@ -201,6 +201,18 @@ template <int DT> __device__ __forceinline__ void store4(void *out, size_t idx, 
     }
 }
 
+// Final output store: the same 4 values to every destination (n_out <= 8), at
+// row b, head (out_head_offset + head).  With peer-mapped destinations (e.g.
+// torch symmetric memory over NVLink) this is the all-gather of head-sharded
+// outputs fused into the epilogue.
+template <int DT>
+__device__ __forceinline__ void store_out(const DecodeParams &p, int b, int head, int d4, float a, float bb, float c,
+                                          float d) {
+    const size_t o = (size_t)b * p.out_row_stride + (size_t)(p.out_head_offset + head) * kHeadDim + d4;
+#pragma unroll 1
+    for (int i = 0; i < p.n_out; ++i) store4<DT>(p.out[i], o, a, bb, c, d);
+}
+
 // ------------------------------------------------------------------ consumers
 // Running online-softmax state of one consumer warp for its share of an item.
 // MMA layout: row = lane/4 (q head of the group), 2 columns per n-tile.
@@ -491,8 +503,7 @@ __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeIte
             c = fmaf(e, v.z, c);
             d = fmaf(e, v.w, d);
         }
-        const size_t o = ((size_t)mg.b * p.num_q_heads + (size_t)mg.g * G + row) * kHeadDim + d4;
-        store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
+        store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
     }
 }
 
@@ -648,8 +659,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     d = fmaf(e, v.w, d);
                 }
                 if (it.part < 0) {
-                    const size_t o = ((size_t)it.b * p.num_q_heads + (size_t)it.g * G + row) * kHeadDim + d4;
-                    store4<DT>(p.out, o, a / den, b / den, c / den, d / den);
+                    store_out<DT>(p, it.b, it.g * G + row, d4, a / den, b / den, c / den, d / den);
                 } else {
                     const size_t o = ((size_t)it.part * G + row) * kHeadDim + d4;
                     *reinterpret_cast<float4 *>(p.part_o + o) = make_float4(a, b, c, d);

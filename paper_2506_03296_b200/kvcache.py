@@ -107,6 +107,22 @@ class PagedKVCache:
         A.apex_decode_attention(self.handle, layer, q.data_ptr(), out.data_ptr(), scale, self._stream())
         return out
 
+    def decode_into(self, layer: int, q, outs, head_offset: int = 0, scale: float | None = None):
+        """Decode writing this handle's q heads into each full-width [B][H_total][D] tensor of
+        `outs` at head `head_offset` (fused all-gather epilogue when `outs` are peer-mapped
+        symmetric buffers of the other ranks)."""
+        B = len(self.batch_seq_ids)
+        self._check_rows(q, B, self.num_q_heads)
+        for o in outs:
+            if o.dim() != 3 or o.shape[0] != B or o.shape[2] != self.head_dim or not o.is_contiguous() \
+                    or o.dtype != torch_dtype(self.dtype):
+                raise ValueError("outs must be contiguous [B][H_total][D] tensors of the cache dtype")
+        if scale is None:
+            scale = 1.0 / math.sqrt(self.head_dim)
+        stride = outs[0].shape[1] * self.head_dim
+        A.apex_decode_attention_ex(self.handle, layer, q.data_ptr(), [o.data_ptr() for o in outs], stride,
+                                   head_offset, scale, self._stream())
+
     def _check_rows(self, t, rows, heads):
         if t.device != self.device or t.dtype != torch_dtype(self.dtype) or not t.is_contiguous():
             raise ValueError(f"expected contiguous {self.dtype} tensor on {self.device}, got {t.dtype} on {t.device}")
