@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
+                    help="head mode: NCCL all_gather_into_tensor, or stores into peers' symmetric memory "
+                         "from the decode epilogue (experimental, needs >= 2 GPUs)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo + APEX_BENCH_SAME_DEVICE=1 runs several ranks on one GPU (logic test only)")
     return ap.parse_args()
@@ -346,8 +349,15 @@ def run_apex(args):
     outs = [torch.empty((B, hq, D), dtype=tdt, device=dev) for _ in range(P)]
     gathered = [None] * P
     head_mode = w.name == "c5" and args.mode == "head" and world > 1
+    fused = head_mode and args.gather == "fused"
     if head_mode:
         from paper_2506_03296_b200.sharding import gather_heads
+    if fused:
+        # all-gather fused into the decode epilogue: every rank stores its head slice
+        # into all ranks' symmetric buffers (peer-mapped over NVLink); experimental
+        from paper_2506_03296_b200 import apex as A
+        from paper_2506_03296_b200.sharding import symmetric_output
+        symm = [symmetric_output((B, w.num_q_heads, D), tdt, dev) for _ in range(P)]
     ones = [1] * B
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K * L)]
 
@@ -359,10 +369,18 @@ def run_apex(args):
             cache.append(p, ks[p], vs[p])
             if timed_idx is not None:
                 ev[timed_idx * L + l][0].record()
-            cache.decode(p, qs[p], out=outs[p])
+            if fused:
+                buf, hdl = symm[p]
+                A.apex_decode_attention_ex(cache.handle, p, qs[p].data_ptr(), list(hdl.buffer_ptrs),
+                                           w.num_q_heads * D, wl["q_off"], 1.0 / D ** 0.5,
+                                           torch.cuda.current_stream(dev).cuda_stream)
+                hdl.barrier(channel=0)               # remote slices landed before anyone reads buf
+                gathered[p] = buf
+            else:
+                cache.decode(p, qs[p], out=outs[p])
             if timed_idx is not None:
                 ev[timed_idx * L + l][1].record()
-            if head_mode:
+            if head_mode and not fused:
                 gathered[p] = gather_heads(outs[p]) if not gloo else gather_heads(outs[p].cpu())
 
     def barrier():
@@ -420,7 +438,7 @@ def run_apex(args):
                          "num_kv_heads": w.num_kv_heads, "head_dim": D, "block_size": 16,
                          "ctx_first_step": {"min": int(ctx0.min()), "mean": float(ctx0.mean()),
                                             "max": int(ctx0.max())},
-                         "parallelism": wl["parallelism"],
+                         "parallelism": wl["parallelism"] + ("+fused_gather" if fused else ""),
                          "l2": f"no flush: each layer-call streams {bytes_per_launch / 2**30:.2f} GiB >> 126 MB L2",
                          "work_items_per_layer": n_items, "split_merges_per_layer": n_merges},
               "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,

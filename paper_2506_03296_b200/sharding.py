@@ -39,6 +39,23 @@ def head_range(num_kv_heads: int, num_q_heads: int, rank: int, world: int):
     return rank * per, (rank + 1) * per, rank * per * g, (rank + 1) * per * g
 
 
+def symmetric_output(shape, dtype, device, group=None):
+    """A full-width output buffer in torch symmetric memory + its rendezvous handle.
+
+    handle.buffer_ptrs holds every rank's (peer-mapped) address of its buffer, to
+    be passed as the destinations of apex_decode_attention_ex: each rank then
+    stores its head slice into all ranks' buffers from the kernel epilogue (the
+    all-gather fused into the decode); handle.barrier()
+    orders those remote stores before the gathered rows are read.
+    NOTE: exercised on one GPU only with local destinations
+    (tests/test_fused_gather_gpu.py); the peer-pointer path needs >= 2 GPUs."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    t = symm_mem.empty(*shape, dtype=dtype, device=device)
+    handle = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+    return t, handle
+
+
 def gather_heads(out_local, group=None):
     """All-gather head-sharded outputs [B][Hq/N][D] -> [B][Hq][D] view.
 
