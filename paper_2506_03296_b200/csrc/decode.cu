@@ -6,12 +6,13 @@
 // memory-bound; FlashDecoding-style split + log-sum-exp merge, cited at P:53).
 //
 // Kernel design:
-//  * persistent grid, 2 CTAs/SM, items pulled longest-first from a device
-//    work queue (atomicAdd), so ragged contexts balance across the 148 SMs;
+//  * persistent grid, 2 CTAs/SM; CTA i starts with item i, then pulls items
+//    longest-first from a device work queue (atomicAdd), so ragged contexts
+//    balance across the 148 SMs;
 //  * warp 0 = producer: reads the block table 32 entries at a time and issues
-//    one TMA (cp.async.bulk.tensor, 128-B swizzle) per K and per V tile of a
-//    (block, kv-head) -- a contiguous 4 KiB (16-bit) / 8 KiB (fp32) tile --
-//    into mbarrier-guarded shared-memory slots;
+//    one TMA (cp.async.bulk.tensor, 128-B swizzle) per (block, kv-head) tile --
+//    its 16 K rows and 16 V rows, contiguous in the interleaved pool: 8 KiB
+//    (16-bit) / 16 KiB (fp32) -- into mbarrier-guarded shared-memory slots;
 //  * warps 1..4 = consumers: tile j of an item goes to consumer j % 4, each
 //    keeps its own running (m, l, O) and the four are merged through shared
 //    memory at the item's end (fixed order => deterministic).  Every consumer
@@ -27,9 +28,12 @@
 //    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
 //    (m, l, unnormalised O) fp32 partials merged in split order -- by a second
-//    small launch (fixed grid, grid-stride over split pairs) in the bandwidth regime, or, in the
-//    latency regime, by the last split of the pair to finish (per-pair arrival
-//    counter) inside this kernel, saving the launch.
+//    small launch (fixed grid, grid-stride over split pairs) in the bandwidth
+//    regime, or, in the latency regime, by the last split of the pair to finish
+//    (per-pair arrival counter) inside this kernel, saving the launch;
+//  * every launch parameter is step-invariant (counts from the device step
+//    header, fixed grids), so the launches are CUDA-graph capturable, and they
+//    use programmatic dependent launch (griddepcontrol) to overlap prologues.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
