@@ -368,8 +368,9 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
 // the device queue (greedy LPT on P CTAs).
 //  * latency regime (T <= 64 P): chunk = ceil(T/P), about one item per CTA, and
 //    the LSE merge is fused into the decode kernel (saves a launch);
-//  * bandwidth regime: chunk = max(4, ceil(T/16P)) -- ~16 items per CTA keeps
+//  * bandwidth regime: chunk = max(16, ceil(T/16P)) -- ~16 items per CTA keeps
 //    the LPT tail short while per-item costs stay ~1% (tools/tune.py sweeps);
+//    the 16-tile floor matters for few long pairs (e.g. batch 1 at 64K tokens);
 //    pairs shorter than the chunk stay whole (e.g. C5: no split at all);
 //  * a forced chunk (apex_kv_set_split) is used as is.
 // A pair cut into >1 pieces gets partial slots and a merge entry.
@@ -402,7 +403,7 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
         chunk = std::max<int64_t>(1, cdiv(T, P));
         latency = true;
     } else {
-        chunk = std::max<int64_t>(4, cdiv(T, 16 * P));
+        chunk = std::max<int64_t>(16, cdiv(T, 16 * P));   // >= 16 tiles: per-item costs stay small
     }
     std::vector<WorkItem> items;
     std::vector<MergeItem> merges;

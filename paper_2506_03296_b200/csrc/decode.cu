@@ -492,10 +492,14 @@ template <int DT, int G>
 __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt) {
     for (int idx = t; idx < G * kHeadDim / 4; idx += nt) {
         const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+        // partial loads are independent across i: unrolled so many are in flight
+        // (long pairs can have hundreds of splits)
         float M = -INFINITY;
+#pragma unroll 8
         for (int i = 0; i < mg.nparts; ++i)
             M = fmaxf(M, __ldcg(p.part_ml + ((size_t)(mg.part0 + i) * G + row) * 2));
         float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll 8
         for (int i = 0; i < mg.nparts; ++i) {
             const size_t pi = (size_t)(mg.part0 + i) * G + row;
             const float2 ml = __ldcg(reinterpret_cast<const float2 *>(p.part_ml + pi * 2));
