@@ -158,8 +158,26 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
    0 = automatic.  A fixed chunk makes results bit-identical across request /
    head sharding (tests).  APEX_EINVAL if not a multiple of block_size or < 0. */
 apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens);
-/* Number of persistent CTAs the planner targets (0 = device default). */
+/* Number of persistent CTAs the planner targets and the decode kernel launches
+   with (0 = device default).  Takes effect at the NEXT apex_kv_alloc. */
 apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas);
+/* Bandwidth-regime scheduling used by the NEXT apex_kv_alloc (ignored in the
+   latency regime and with a forced split chunk):
+     dyn_permille = -1: every (row, kv-head) pair cut into ~16 items per CTA,
+                        pulled longest-first from a device queue (FlashDecoding-
+                        style dynamic split);
+     dyn_permille = -2: "guided" (default): as -1 with ~8 items per CTA, except that
+                        the pairs holding the last 10% / 5% / 2% of the tiles are
+                        cut into 1/2, 1/4, 1/8-size items, so the queue ends with
+                        small items;
+     dyn_permille in [0, 1000]: "stream-K" -- the first (1000 - dyn_permille)
+                        permille of the tiles, in (row, kv-head, block) order,
+                        are cut into one contiguous static range per CTA (no
+                        queue traffic, ~T/P tiles each); the rest are small items
+                        pulled from the queue after a CTA's static range.
+   Default: the automatic choice documented in DESIGN.md.  APEX_EINVAL outside
+   [-2, 1000]. */
+apex_status apex_kv_set_sched(apex_kv *kv, int32_t dyn_permille);
 int32_t apex_kv_num_free_blocks(const apex_kv *kv);
 /* len and block ids (table order) of a live sequence; *n_blocks may exceed cap
    (then only cap ids are written). */
@@ -171,6 +189,12 @@ apex_status apex_kv_last_slots(const apex_kv *kv, int32_t *slots, int32_t cap, i
    block, n blocks, partial slot or -1, seq id}, in execution-priority order */
 apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t *n_items,
                          int32_t *n_merges);
+
+/* last alloc's per-CTA static ranges: *n = grid + 1 entries cta_begin[] (CTA c
+   runs items [cta_begin[c], cta_begin[c+1]) of apex_kv_plan's list first; items
+   from cta_begin[grid] on are pulled from the device queue).  At most cap
+   entries are written. */
+apex_status apex_kv_plan_ranges(const apex_kv *kv, int32_t *cta_begin, int32_t cap, int32_t *n);
 
 /* Kernel launches the next apex_decode_attention will issue for the last alloc's
    plan: 1 (decode kernel; LSE merge fused in-kernel, latency regime) or 2

@@ -22,8 +22,8 @@ DTYPE_CODE = {"f32": APEX_F32, "f16": APEX_F16, "bf16": APEX_BF16}
 
 # every symbol the public headers declare (checked by tests/test_host_core.py)
 EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex_kv_alloc", "apex_kv_release",
-           "apex_kv_append", "apex_decode_attention", "apex_kv_set_split", "apex_kv_set_grid",
-           "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan",
+           "apex_kv_append", "apex_decode_attention", "apex_kv_set_split", "apex_kv_set_grid", "apex_kv_set_sched",
+           "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan", "apex_kv_plan_ranges",
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
            "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex"]
 STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
@@ -77,10 +77,12 @@ def lib():
             "apex_decode_attention": (c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_float, c_void_p]),
             "apex_kv_set_split": (c_int, [c_void_p, c_int32]),
             "apex_kv_set_grid": (c_int, [c_void_p, c_int32]),
+            "apex_kv_set_sched": (c_int, [c_void_p, c_int32]),
             "apex_kv_num_free_blocks": (c_int32, [c_void_p]),
             "apex_kv_seq_info": (c_int, [c_void_p, c_int32, P32, P32, c_int32, P32]),
             "apex_kv_last_slots": (c_int, [c_void_p, P32, c_int32, P32]),
             "apex_kv_plan": (c_int, [c_void_p, P32, c_int32, P32, P32]),
+            "apex_kv_plan_ranges": (c_int, [c_void_p, P32, c_int32, P32]),
             "apex_cost_create": (c_int, [P32, c_int32, POINTER(c_int64), c_int32, POINTER(c_double),
                                          POINTER(c_void_p)]),
             "apex_predict_time": (c_int, [c_void_p, c_int32, c_int64, POINTER(c_double)]),
@@ -157,6 +159,10 @@ def apex_kv_set_grid(kv: int, ctas: int) -> None:
     _check(lib().apex_kv_set_grid(kv, int(ctas)))
 
 
+def apex_kv_set_sched(kv: int, dyn_permille: int) -> None:
+    _check(lib().apex_kv_set_sched(kv, int(dyn_permille)))
+
+
 def apex_kv_num_free_blocks(kv: int) -> int:
     return int(lib().apex_kv_num_free_blocks(kv))
 
@@ -176,6 +182,15 @@ def apex_kv_last_slots(kv: int):
     buf = (c_int32 * max(n.value, 1))()
     _check(lib().apex_kv_last_slots(kv, buf, n.value, ctypes.byref(n)))
     return list(buf[:n.value])
+
+
+def apex_kv_plan_ranges(kv: int):
+    """Per-CTA static item ranges of the last plan: list of grid + 1 offsets."""
+    n = c_int32(0)
+    _check(lib().apex_kv_plan_ranges(kv, None, 0, ctypes.byref(n)))
+    buf = (c_int32 * n.value)()
+    _check(lib().apex_kv_plan_ranges(kv, buf, n.value, ctypes.byref(n)))
+    return list(buf)
 
 
 def apex_kv_plan(kv: int):

@@ -48,6 +48,9 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int elem_bytes(apex_dtype dt) { return dt == APEX_F32 ? 4 : 2; }
 
+// default bandwidth-regime schedule (apex_kv_set_sched): see DESIGN.md section 7
+constexpr int32_t kDefaultDynPermille = -2;
+
 bool desc_host_only(const apex_kv_desc *d) { return d->kv_pool == nullptr && d->block_table == nullptr; }
 
 int query_sm_count(bool host_only) {
@@ -74,12 +77,14 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     const int G = d->num_q_heads / d->num_kv_heads;
     const int64_t pairs = (int64_t)d->max_batch * d->num_kv_heads;
     // auto planner: items <= pairs + 64 * grid (small pieces) ; grid <= 4 * SMs
-    w.max_items = (int32_t)std::min<int64_t>(pairs + 64LL * 4 * sm_count + 64, 1 << 24);
+    // (stream-K: <= pairs + grid static cuts + pairs + 8 * grid dynamic pieces)
+    w.max_items = (int32_t)std::min<int64_t>(2 * pairs + 64LL * 4 * sm_count + 64, 1 << 24);
     w.max_merges = (int32_t)pairs;
     w.max_bt_delta = (int32_t)(cdiv(d->max_new_tokens, d->block_size) + d->max_batch);
     // upload region, fixed offsets: [StepHeader | work items | merges | tail: slots,
     // block-table deltas, length deltas (packed)]; the kernels' pointers into it never move
-    w.o_items = 256;
+    // header | cta_begin[grid + 1] (grid <= 4 * SMs) | items ...
+    w.o_items = align_up(apex::kCtaBeginOffset + sizeof(int32_t) * (4 * (size_t)sm_count + 1), 256);
     w.o_merges = w.o_items + align_up(sizeof(WorkItem) * (size_t)w.max_items, 256);
     w.o_tail = w.o_merges + align_up(sizeof(MergeItem) * (size_t)w.max_merges, 256);
     size_t up = w.o_tail;
@@ -192,6 +197,10 @@ struct apex_kv {
     WsLayout ws;
     int32_t forced_chunk_blocks = 0;
     int32_t grid_override = 0;
+    int32_t dyn_permille = kDefaultDynPermille;   // apex_kv_set_sched
+    int32_t guided[4] = {8, 900, 950, 980};       // guided: T/(g0 P) chunk, halved from permille g1, g2, g3
+    int32_t plan_grid = 0;                        // CTAs the last plan was made for (= launch grid)
+    std::vector<int32_t> cta_begin;               // [plan_grid + 1]
 
     struct Seq {
         bool live = false;
@@ -316,8 +325,15 @@ apex_status apex_kv_set_split(apex_kv *kv, int32_t chunk_tokens) {
 }
 
 apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas) {
-    if (!kv || ctas < 0) return fail(APEX_EINVAL, "bad grid override");
+    if (!kv || ctas < 0 || ctas > 4 * kv->sm_count) return fail(APEX_EINVAL, "bad grid override");
     kv->grid_override = ctas;
+    return APEX_OK;
+}
+
+apex_status apex_kv_set_sched(apex_kv *kv, int32_t dyn_permille) {
+    if (!kv || dyn_permille < -2 || dyn_permille > 1000)
+        return fail(APEX_EINVAL, "dyn_permille %d not in [-2, 1000]", dyn_permille);
+    kv->dyn_permille = dyn_permille;
     return APEX_OK;
 }
 
@@ -346,6 +362,15 @@ apex_status apex_kv_last_slots(const apex_kv *kv, int32_t *slots, int32_t cap, i
     if (n) *n = (int32_t)kv->slots.size();
     if (slots)
         for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)kv->slots.size()); ++i) slots[i] = kv->slots[i];
+    return APEX_OK;
+}
+
+apex_status apex_kv_plan_ranges(const apex_kv *kv, int32_t *cta_begin, int32_t cap, int32_t *n) {
+    if (!kv || !kv->have_step) return fail(APEX_EINVAL, "no step allocated");
+    if (n) *n = (int32_t)kv->cta_begin.size();
+    if (cta_begin)
+        for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)kv->cta_begin.size()); ++i)
+            cta_begin[i] = kv->cta_begin[i];
     return APEX_OK;
 }
 
@@ -382,6 +407,54 @@ void pieces_of(int32_t nblk, int64_t chunk, std::vector<int32_t> &out) {
 }
 }  // namespace
 
+// Stream-K variant of the bandwidth regime (apex_kv_set_sched, dyn_permille >= 0):
+// the tiles, flattened in (row, kv head, block) order, are dealt out as one
+// contiguous static range of ~T_static/P tiles per CTA -- a CTA's range covers
+// the tail of one pair, whole pairs and the head of the next, so it runs only a
+// few items and never touches the queue; pairs cut at a range boundary are
+// merged like any split pair.  The last dyn_permille of the tiles are cut into
+// small items (<= 8 per CTA) pulled from the queue by CTAs that finish their
+// range early: they absorb SM-to-SM bandwidth differences.
+namespace {
+struct Piece {
+    int32_t cta;    // static owner, or -1 for the dynamic queue
+    int32_t blk0, nblk;
+};
+}  // namespace
+
+static void plan_streamk(const std::vector<int32_t> &nblks, int32_t Hkv, int64_t P, int64_t T, int32_t dyn_permille,
+                         std::vector<std::vector<Piece>> &pair_pieces) {
+    const int64_t T_dyn = T * dyn_permille / 1000, T_st = T - T_dyn;
+    const int64_t dchunk = std::max<int64_t>(16, cdiv(T_dyn, 8 * P));
+    const int64_t base = T_st / P, rem = T_st % P;
+    auto quota = [&](int64_t c) { return base + (c < rem ? 1 : 0); };
+    int64_t c = 0, left = quota(0);
+    while (c < P && left == 0) left = quota(++c);
+    const int32_t B = (int32_t)nblks.size();
+    pair_pieces.assign((size_t)B * Hkv, {});
+    std::vector<int32_t> dp;
+    for (int32_t b = 0; b < B; ++b)
+        for (int32_t g = 0; g < Hkv; ++g) {
+            auto &pp = pair_pieces[(size_t)b * Hkv + g];
+            int32_t blk = 0, r = nblks[b];
+            while (r > 0 && c < P) {
+                const int32_t take = (int32_t)std::min<int64_t>(r, left);
+                pp.push_back({(int32_t)c, blk, take});
+                blk += take;
+                r -= take;
+                left -= take;
+                while (c < P && left == 0) left = quota(++c);
+            }
+            if (r > 0) {                               // beyond the static share: dynamic pieces
+                pieces_of(r, dchunk, dp);
+                for (int32_t n : dp) {
+                    pp.push_back({-1, blk, n});
+                    blk += n;
+                }
+            }
+        }
+}
+
 static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     const int32_t Hkv = kv->d.num_kv_heads, B = (int32_t)lens.size();
     const int64_t P = std::max<int64_t>(1, kv->grid_override > 0
@@ -395,42 +468,91 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
         T += (int64_t)nblks[b] * Hkv;
 
     }
-    int64_t chunk;
-    bool latency = false;
+    int64_t chunk = 0;
+    bool latency = false, streamk = false;
     if (kv->forced_chunk_blocks > 0) {
         chunk = kv->forced_chunk_blocks;
     } else if (T <= 64 * P) {
         chunk = std::max<int64_t>(1, cdiv(T, P));
         latency = true;
+    } else if (kv->dyn_permille >= 0) {
+        streamk = true;
     } else {
         chunk = std::max<int64_t>(16, cdiv(T, 16 * P));   // >= 16 tiles: per-item costs stay small
     }
-    std::vector<WorkItem> items;
-    std::vector<MergeItem> merges;
-    std::vector<int32_t> pc;
-    int32_t parts = 0;
-    for (int32_t b = 0; b < B; ++b) {
-        pieces_of(nblks[b], chunk, pc);
-        const bool split = pc.size() > 1;
-        for (int32_t g = 0; g < Hkv; ++g) {
-            const int32_t mg = split ? (int32_t)merges.size() : -1;
-            if (split) merges.push_back({b, g, parts, (int32_t)pc.size()});
-            int32_t blk = 0;
-            for (size_t i = 0; i < pc.size(); ++i) {
-                items.push_back({b, g, blk, pc[i], split ? parts + (int32_t)i : -1, kv->batch_seq[b], lens[b], mg});
-                blk += pc[i];
+    // pieces of every (row, kv head) pair, in pair order
+    std::vector<std::vector<Piece>> pair_pieces;
+    if (streamk) {
+        plan_streamk(nblks, Hkv, P, T, kv->dyn_permille, pair_pieces);
+    } else {
+        pair_pieces.assign((size_t)B * Hkv, {});
+        std::vector<int32_t> pc;
+        // guided (apex_kv_set_sched(-2)): the pairs holding the last fractions of the
+        // tiles (flattened order) are cut into halved, quartered, ... chunks, so the
+        // queue (longest first) ends with small items and the CTAs finish together
+        const bool guided = !latency && kv->forced_chunk_blocks == 0 && kv->dyn_permille == -2;
+        if (const char *e = guided ? std::getenv("APEX_GUIDED") : nullptr)   // tuning aid: "div,pm1,pm2,pm3"
+            std::sscanf(e, "%d,%d,%d,%d", &kv->guided[0], &kv->guided[1], &kv->guided[2], &kv->guided[3]);
+        if (guided) chunk = std::max<int64_t>(16, cdiv(T, (int64_t)kv->guided[0] * P));
+        int64_t pos = 0;
+        for (int32_t b = 0; b < B; ++b) {
+            for (int32_t g = 0; g < Hkv; ++g) {
+                if (g == 0 || guided) {
+                    int64_t c = chunk;
+                    for (int k = 1; guided && k < 4; ++k)
+                        if (pos * 1000 >= (int64_t)kv->guided[k] * T) c = std::max<int64_t>(8, chunk >> k);
+                    pieces_of(nblks[b], c, pc);
+                }
+                pos += nblks[b];
+                int32_t blk = 0;
+                for (int32_t n : pc) {
+                    pair_pieces[(size_t)b * Hkv + g].push_back({-1, blk, n});
+                    blk += n;
+                }
             }
-            if (split) parts += (int32_t)pc.size();
         }
     }
-    if ((int64_t)items.size() > kv->ws.max_items)
+    std::vector<std::vector<WorkItem>> st_items(streamk ? P : 0);
+    std::vector<WorkItem> dyn;
+    std::vector<MergeItem> merges;
+    int32_t parts = 0;
+    size_t n_items = 0;
+    for (int32_t b = 0; b < B; ++b)
+        for (int32_t g = 0; g < Hkv; ++g) {
+            const auto &pp = pair_pieces[(size_t)b * Hkv + g];
+            const bool split = pp.size() > 1;
+            const int32_t mg = split ? (int32_t)merges.size() : -1;
+            if (split) merges.push_back({b, g, parts, (int32_t)pp.size()});
+            for (size_t i = 0; i < pp.size(); ++i) {
+                const WorkItem w{b, g, pp[i].blk0, pp[i].nblk, split ? parts + (int32_t)i : -1, kv->batch_seq[b],
+                                 lens[b], mg};
+                (pp[i].cta >= 0 ? st_items[pp[i].cta] : dyn).push_back(w);
+            }
+            if (split) parts += (int32_t)pp.size();
+            n_items += pp.size();
+        }
+    if ((int64_t)n_items > kv->ws.max_items)
         return fail(APEX_EINVAL, "split chunk of %lld tokens yields %zu work items > workspace capacity %d",
-                    (long long)chunk * kv->d.block_size, items.size(), kv->ws.max_items);
-    std::stable_sort(items.begin(), items.end(),
-                     [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
+                    (long long)chunk * kv->d.block_size, n_items, kv->ws.max_items);
+    std::stable_sort(dyn.begin(), dyn.end(), [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
+    std::vector<WorkItem> items;
+    items.reserve(n_items);
+    kv->cta_begin.assign((size_t)P + 1, 0);
+    if (streamk) {
+        for (int64_t c = 0; c < P; ++c) {
+            kv->cta_begin[c] = (int32_t)items.size();
+            items.insert(items.end(), st_items[c].begin(), st_items[c].end());
+        }
+        kv->cta_begin[P] = (int32_t)items.size();
+    } else {
+        // CTA c starts with item c (no queue round trip on the launch path), then the queue
+        for (int64_t c = 0; c <= P; ++c) kv->cta_begin[c] = (int32_t)std::min<int64_t>(c, (int64_t)dyn.size());
+    }
+    items.insert(items.end(), dyn.begin(), dyn.end());
     kv->items.swap(items);
     kv->merges.swap(merges);
     kv->fuse_merge = latency;
+    kv->plan_grid = (int32_t)P;
     return APEX_OK;
 }
 
@@ -508,6 +630,7 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     uint8_t *host = kv->staging[r];
     const apex::StepHeader hdr{(int32_t)kv->items.size(), (int32_t)kv->merges.size(), (int32_t)rows, 0};
     std::memcpy(host, &hdr, sizeof hdr);
+    std::memcpy(host + apex::kCtaBeginOffset, kv->cta_begin.data(), sizeof(int32_t) * kv->cta_begin.size());
     const size_t items_bytes = sizeof(WorkItem) * kv->items.size();
     const size_t merges_bytes = sizeof(MergeItem) * kv->merges.size();
     std::memcpy(host + kv->ws.o_items, kv->items.data(), items_bytes);
@@ -600,6 +723,7 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
     uint8_t *ws = (uint8_t *)kv->d.workspace;
     uint8_t *up = ws + kv->ws.upload;
     p.hdr = (const apex::StepHeader *)up;
+    p.cta_begin = (const int32_t *)(up + apex::kCtaBeginOffset);
     p.items = (const WorkItem *)(up + kv->ws.o_items);
     p.merges = (const MergeItem *)(up + kv->ws.o_merges);
     p.part_o = (float *)(ws + kv->ws.part_o);
@@ -615,7 +739,7 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
     p.fuse_merge = kv->fuse_merge ? 1 : 0;
     // fixed persistent grid (CTAs without an item exit at once): every launch parameter is
     // step-invariant, so the per-layer launches can be captured in a CUDA graph
-    const int grid = apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count);
+    const int grid = kv->plan_grid;   // cta_begin has plan_grid + 1 entries
     cudaError_t e = apex::launch_decode(kv->d.dtype, kv->group, kv->tmaps[layer], p, grid, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_decode_attention");
 }

@@ -45,6 +45,11 @@ struct __align__(16) StepHeader {
     int32_t n_rows;       // new-token rows of the step (append)
     int32_t pad;
 };
+// Right after the header (at byte kCtaBeginOffset of the upload region): int32
+// cta_begin[grid + 1].  CTA c first runs items [cta_begin[c], cta_begin[c+1])
+// (its static range), then pulls items cta_begin[grid] + atomicAdd(queue) until
+// the list ends.
+constexpr int kCtaBeginOffset = 16;
 
 struct DecodeParams {
     const void *q;             // [B][Hq][D]
@@ -60,6 +65,7 @@ struct DecodeParams {
     int32_t *counters;         // [2]: work-queue head, CTAs done
     int32_t *merge_counters;   // [n_merges]: split items finished per pair (left at 0)
     const StepHeader *hdr;     // this step's counts (device, written by apex_kv_alloc's upload)
+    const int32_t *cta_begin;  // [grid + 1] static item ranges, then the dynamic queue base
     int32_t merge_grid;        // fixed grid of the merge kernel (grid-stride over hdr->n_merges)
     int32_t max_blocks_per_seq;
     int32_t num_q_heads;

@@ -40,6 +40,18 @@
 #include "apex_internal.h"
 
 namespace apex {
+#ifdef APEX_TRACE
+// timing instrumentation (tuning builds only): globaltimer stamps per CTA
+__device__ unsigned long long g_apex_trace[1024][16];
+__device__ __forceinline__ void trace(int ev) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_apex_trace[blockIdx.x][ev] = t;
+}
+#define TRACE(ev) trace(ev)
+#else
+#define TRACE(ev) ((void)0)
+#endif
 namespace {
 
 #ifndef APEX_NC
@@ -51,11 +63,14 @@ namespace {
 #ifndef APEX_EARLY_RELEASE
 #define APEX_EARLY_RELEASE 0
 #endif
+#ifndef APEX_MAX_SLOTS
+#define APEX_MAX_SLOTS 24
+#endif
 #ifndef APEX_L2_EVICT_FIRST
 #define APEX_L2_EVICT_FIRST 0
 #endif
 constexpr int NC = APEX_NC;              // consumer warps
-constexpr int NTHREADS = 32 * (NC + 1);
+constexpr int NTHREADS = 32 * (NC + 1);   // producer warp + NC consumer warps
 constexpr int IR = 4;                    // item-ring entries
 constexpr int CTAS_PER_SM = APEX_CTAS_PER_SM;
 constexpr int kTileRows = kBlock;        // 16 tokens per tile
@@ -78,7 +93,7 @@ template <int DT, int G> struct Cfg {
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
     static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
-    static constexpr int SW = (S0 > 24 ? 24 : S0) / NC;      // slots per consumer warp
+    static constexpr int SW = (S0 > APEX_MAX_SLOTS ? APEX_MAX_SLOTS : S0) / NC;   // slots per consumer warp
     static constexpr int STAGES = SW * NC;
     static constexpr int TILES = STAGES * 2 * TILE;
     static constexpr int BARS = (2 * STAGES + 2 * IR) * 8;
@@ -225,14 +240,14 @@ template <int DT, int G> struct MmaConsumer {
     float o[16][4];             // O accumulators, n-tile nd covers dims nd*8..nd*8+7
     float m, l;                 // running max (log2 units) and this thread's partial sum
 
-    __device__ __forceinline__ void begin(const void *q, const DecodeParams &p, const WorkItem &it, int lane) {
+    // qg: the G q rows of the item's kv head (global memory, or the item's smem q slot)
+    __device__ __forceinline__ void begin(const uint8_t *qg, const DecodeParams &, int lane) {
         const int row = lane >> 2, tid = lane & 3;
-        const uint32_t *qrow = reinterpret_cast<const uint32_t *>(
-            static_cast<const uint16_t *>(q) + ((size_t)it.b * p.num_q_heads + (size_t)it.g * G + row) * kHeadDim);
+        const uint32_t *qrow = reinterpret_cast<const uint32_t *>(qg + (size_t)row * kHeadDim * 2);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-            qa[kk][0] = row < G ? __ldg(qrow + kk * 8 + tid) : 0u;
-            qa[kk][1] = row < G ? __ldg(qrow + kk * 8 + 4 + tid) : 0u;
+            qa[kk][0] = row < G ? qrow[kk * 8 + tid] : 0u;
+            qa[kk][1] = row < G ? qrow[kk * 8 + 4 + tid] : 0u;
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -346,24 +361,24 @@ template <int DT> struct SimtConsumer {
     float o[8];                 // 16-bit: 8 dims; fp32: 4 dims (o[0..3])
     float m, l;                 // l: per-lane partial of sum p (lanes 0..15 distinct)
 
-    __device__ __forceinline__ void begin(const void *q, const DecodeParams &p, const WorkItem &it, int lane) {
+    __device__ __forceinline__ void begin(const uint8_t *qg, const DecodeParams &p, int lane) {
         const int hh = lane >> 4;
-        const size_t base = ((size_t)it.b * p.num_q_heads + it.g) * kHeadDim + hh * 64;
+        const size_t base = (size_t)hh * 64;
         if constexpr (F32) {
-            const float4 *src = reinterpret_cast<const float4 *>(static_cast<const float *>(q) + base);
+            const float4 *src = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(qg) + base);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                float4 v = __ldg(src + i);
+                float4 v = src[i];
                 qv[4 * i] = v.x * p.scale_log2;
                 qv[4 * i + 1] = v.y * p.scale_log2;
                 qv[4 * i + 2] = v.z * p.scale_log2;
                 qv[4 * i + 3] = v.w * p.scale_log2;
             }
         } else {
-            const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(q) + base);
+            const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint16_t *>(qg) + base);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                uint4 v = __ldg(src + i);
+                uint4 v = src[i];
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -488,31 +503,116 @@ template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
 // log-sum-exp merge of one split (b, g) pair, partials combined in split order:
 // M = max m_i, out = sum 2^(m_i-M) O_i / sum 2^(m_i-M) l_i.  Partials written by
 // other CTAs are read through L2 (ld.global.cg).
-template <int DT, int G>
-__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt) {
-    for (int idx = t; idx < G * kHeadDim / 4; idx += nt) {
-        const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
-        // partial loads are independent across i: unrolled so many are in flight
-        // (long pairs can have hundreds of splits)
+//
+// Parallel form (nparts * G * 2 + 2 G floats of scratch `sm` available): the
+// pair's (m, l) are contiguous (consecutive partial slots), so all threads load
+// them in ONE round trip into smem; per-row max and weights w_i = 2^(m_i - M)
+// are formed there; then thread (output float4 o, part group gr) accumulates
+// w_i O_i over parts i = gr, gr + ngr, ... (independent loads, many in flight),
+// and part groups are summed through smem in fixed order.  This replaces a
+// per-thread serial loop whose dependent batches of loads made a 37-way merge
+// cost ~7 us and a 256-way merge ~150 us.  `sync` is a barrier over the nt
+// participating threads; `red` (ngr > 1 only) holds ngr * G * 32 float4.
+template <int DT, int G, typename Sync>
+__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt, float *sm,
+                                           int sm_cap, float4 *red, int red_cap, Sync sync) {
+    const int np = mg.nparts, nml = np * G;
+    constexpr int NOUT = G * kHeadDim / 4;                    // float4 outputs of the pair
+    const float2 *ml = reinterpret_cast<const float2 *>(p.part_ml) + (size_t)mg.part0 * G;
+    if (2 * nml + 2 * G > sm_cap) {
+        // too many parts for the scratch: serial form
+        for (int idx = t; idx < NOUT; idx += nt) {
+            const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+            float M = -INFINITY;
+#pragma unroll 8
+            for (int i = 0; i < np; ++i) M = fmaxf(M, __ldcg(ml + (size_t)i * G + row).x);
+            float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < np; ++i) {
+                const size_t pi = (size_t)(mg.part0 + i) * G + row;
+                const float2 v2 = __ldcg(ml + (size_t)i * G + row);
+                const float e = ex2_diff(v2.x, M);
+                const float4 v = __ldcg(reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4));
+                den = fmaf(e, v2.y, den);
+                a = fmaf(e, v.x, a);
+                b = fmaf(e, v.y, b);
+                c = fmaf(e, v.z, c);
+                d = fmaf(e, v.w, d);
+            }
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
+        }
+        return;
+    }
+    float *sw = sm, *sl = sm + nml, *sM = sm + 2 * nml, *sden = sM + G;
+    if (t == 0 && !red) TRACE(12);
+    for (int i = t; i < nml; i += nt) {
+        const float2 v = __ldcg(ml + i);
+        sw[i] = v.x;
+        sl[i] = v.y;
+    }
+    sync();
+    if (t == 0 && !red) TRACE(13);
+    const int lane = t & 31, wid = t >> 5, nw = nt >> 5;
+    for (int row = wid; row < G; row += nw) {                 // per-row max, then weights and denominator
         float M = -INFINITY;
-#pragma unroll 8
-        for (int i = 0; i < mg.nparts; ++i)
-            M = fmaxf(M, __ldcg(p.part_ml + ((size_t)(mg.part0 + i) * G + row) * 2));
-        float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
-#pragma unroll 8
-        for (int i = 0; i < mg.nparts; ++i) {
-            const size_t pi = (size_t)(mg.part0 + i) * G + row;
-            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(p.part_ml + pi * 2));
-            const float e = ex2_diff(ml.x, M);
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4));
-            den = fmaf(e, ml.y, den);
+        for (int i = lane; i < np; i += 32) M = fmaxf(M, sw[i * G + row]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        float den = 0.f;
+        for (int i = lane; i < np; i += 32) {
+            const float e = ex2_diff(sw[i * G + row], M);
+            sw[i * G + row] = e;
+            den = fmaf(e, sl[i * G + row], den);
+        }
+        // fixed-order sum: lane partials combined by a fixed butterfly (deterministic)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+        if (lane == 0) {
+            sM[row] = M;
+            sden[row] = den;
+        }
+    }
+    sync();
+    if (t == 0 && !red) TRACE(14);
+    const int ngr = red ? min(max(1, nt / NOUT), red_cap / NOUT) : 1;
+    for (int idx = t; idx < NOUT * ngr; idx += nt) {
+        const int o = idx % NOUT, gr = idx / NOUT;
+        const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
+        float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+        const float *po = p.part_o + ((size_t)mg.part0 * G + row) * kHeadDim + d4;
+#pragma unroll 16
+        for (int i = gr; i < np; i += ngr) {
+            const float e = sw[i * G + row];
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + (size_t)i * G * kHeadDim));
             a = fmaf(e, v.x, a);
             b = fmaf(e, v.y, b);
             c = fmaf(e, v.z, c);
             d = fmaf(e, v.w, d);
         }
-        store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
+        if (ngr == 1) {
+            const float den = sden[row];
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
+        } else {
+            red[gr * NOUT + o] = make_float4(a, b, c, d);
+        }
     }
+    if (ngr > 1) {
+        sync();
+        for (int o = t; o < NOUT; o += nt) {
+            const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
+            float4 acc = red[o];
+            for (int gr = 1; gr < ngr; ++gr) {
+                const float4 v = red[gr * NOUT + o];
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+            const float den = sden[row];
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, acc.x / den, acc.y / den, acc.z / den, acc.w / den);
+        }
+    }
+    sync();                                                    // scratch reusable by the caller
 }
 
 // ------------------------------------------------------------------ decode kernel
@@ -536,6 +636,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     const uint32_t ifull0 = empty0 + 8 * STAGES, iempty0 = ifull0 + 8 * IR;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TRACE(0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(full0 + 8 * i, 1);
@@ -554,21 +655,26 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     // may be scheduled now; they wait on their own griddepcontrol.wait.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) TRACE(1);
 
     if (warp == 0) {
         // ================= producer: work queue + block table + TMA =================
-        // (Measured alternatives -- control loads run ahead, lane-0-only tile loop,
-        // block-table chunk prefetch -- were all slower on B200.)
+        // Measured alternatives: running the next item's control
+        // loads ahead in this warp (7-13% slower: the dependent round trips then stall
+        // the TMA stream mid-item), and a separate scheduler warp feeding item, q and
+        // block ids through shared memory (no faster at the default split, +1 warp).
         const int n_items = p.hdr->n_items;    // this step's work-list length (device header)
+        int s_next = __ldg(p.cta_begin + blockIdx.x);
+        const int s_end = __ldg(p.cta_begin + blockIdx.x + 1), q_base = __ldg(p.cta_begin + gridDim.x);
         int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
 #pragma unroll
         for (int q = 0; q < NC; ++q) pc[q] = 0;
         for (int k = 0;; ++k) {
-            // first item is static (CTA i takes item i: no queue round trip on the
-            // launch-latency path); later items come from the queue, offset by grid
-            int idx = blockIdx.x;
-            if (k > 0) {
-                if (lane == 0) idx = (int)gridDim.x + atomicAdd(p.counters, 1);
+            int idx;
+            if (s_next < s_end) {
+                idx = s_next++;
+            } else {
+                if (lane == 0) idx = q_base + atomicAdd(p.counters, 1);
                 idx = __shfl_sync(0xffffffffu, idx, 0);
             }
             const int slot = k % IR, use = k / IR;
@@ -585,11 +691,18 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             if (lane == 0) {
                 ring[slot].it = it;
                 mbar_arrive(ifull0 + 8 * slot);
+                if (k == 0) TRACE(2);
             }
             const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
                 const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
+#ifdef APEX_TRACE
+                if (k == 0 && j0 == 0) {
+                    __shfl_sync(0xffffffffu, my, 0);
+                    if (lane == 0) TRACE(3);
+                }
+#endif
                 for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
                     const int w = (j0 + jj) % NC;
@@ -607,9 +720,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                         if (p.tma_segs == 1) {
                             tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
                         } else {
-                            for (int sg = 0; sg < p.tma_segs; ++sg) {
+                            for (int sg = 0; sg < p.tma_segs; ++sg)
                                 tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
-                            }
                         }
                     }
                 }
@@ -617,6 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         }
         // last CTA out resets the queue for the next launch on this layer
         if (lane == 0) {
+            TRACE(4);
             __threadfence();
             if (atomicAdd(p.counters + 1, 1) == (int)gridDim.x - 1) {
                 atomicExch(p.counters, 0);
@@ -632,14 +745,18 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             const int slot = k % IR, use = k / IR;
             mbar_wait(ifull0 + 8 * slot, use & 1);
             const WorkItem it = ring[slot].it;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(iempty0 + 8 * slot);
             if (it.nblk == 0) break;
-            st.begin(p.q, p, it, lane);
+            st.begin(static_cast<const uint8_t *>(p.q) +
+                         ((size_t)it.b * p.num_q_heads + (size_t)it.g * G) * kHeadDim * C::ES, p, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(iempty0 + 8 * slot);   // item and q slot read
             for (int j = wc; j < it.nblk; j += NC) {
                 const int s = wc * C::SW + mc % C::SW, u = mc / C::SW;
                 ++mc;
                 mbar_wait(full0 + 8 * s, u & 1);
+#ifdef APEX_TRACE
+                if (k == 0 && j == 0 && lane == 0 && wc == 0) TRACE(5);
+#endif
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;
                 st.tile(kt, kt + kVOff, valid, p.scale_log2, lane, [&] {
@@ -647,8 +764,14 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (lane == 0) mbar_arrive(empty0 + 8 * s);   // release it to the producer
                 });
             }
+#ifdef APEX_TRACE
+            if (k == 0 && lane == 0 && wc == 0) TRACE(6);
+#endif
             st.finish(cb_o, cb_m, cb_l, wc, lane);
             named_bar_sync(1, NC * 32);
+#ifdef APEX_TRACE
+            if (k == 0 && threadIdx.x == 32) TRACE(7);
+#endif
             // ---- merge the NC warp states (fixed order), 4 dims per step
             for (int idx = threadIdx.x - 32; idx < G * kHeadDim / 4; idx += NC * 32) {
                 const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
@@ -674,6 +797,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (d4 == 0) *reinterpret_cast<float2 *>(p.part_ml + ((size_t)it.part * G + row) * 2) = make_float2(M, den);
                 }
             }
+#ifdef APEX_TRACE
+            if (k == 0 && threadIdx.x == 32) TRACE(8);
+#endif
             if (FUSE && it.part >= 0) {
                 // last-arriving split of this (b, g) pair merges all its partials (fused LSE merge)
                 __threadfence();
@@ -685,23 +811,39 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     *merge_flag = last;
                 }
                 named_bar_sync(1, NC * 32);
+#ifdef APEX_TRACE
+                if (k == 0 && threadIdx.x == 32) TRACE(9);
+#endif
                 if (*merge_flag) {
                     __threadfence();
-                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32);
+                    // scratch: the per-warp O buffer (free after this item's warp merge)
+                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32, cb_o, NC * G * kHeadDim,
+                                      nullptr, 0, [] { named_bar_sync(1, NC * 32); });
+#ifdef APEX_TRACE
+                    named_bar_sync(1, NC * 32);
+                    if (threadIdx.x == 32) TRACE(10);
+#endif
                 }
             }
             named_bar_sync(1, NC * 32);
         }
+        if (threadIdx.x == 32) TRACE(11);
     }
 }
 
 // log-sum-exp merge of split pairs as its own launch (bandwidth regime): one CTA
 // per (b, g) pair, so merging never stalls a decode CTA's TMA stream.
+constexpr int kMergeThreads = 256;
+constexpr int kMergeScratch = 6144;                        // floats: (m, l) of up to 3072 / G parts
 template <int DT, int G>
-__global__ void __launch_bounds__(128) apex_merge_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeParams p) {
+    __shared__ float sm[kMergeScratch];
+    __shared__ float4 red[kMergeThreads];                   // part-group partial sums (G * 32 * ngr float4)
     asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
     const int n = p.hdr->n_merges;                          // fixed grid, grid-stride over this step's pairs
-    for (int i = blockIdx.x; i < n; i += gridDim.x) merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x);
+    for (int i = blockIdx.x; i < n; i += gridDim.x)
+        merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x, sm, kMergeScratch, red, kMergeThreads,
+                          [] { __syncthreads(); });
 }
 
 template <int DT, int G> cudaError_t prepare() {
@@ -743,10 +885,21 @@ cudaError_t launch(const TmaMap &tm, const DecodeParams &p, int grid, cudaStream
     }
     // launched whenever merges are not fused, even if this step has none (it then
     // exits at once): the launch sequence never depends on the step's plan
-    return launch_pdl(apex_merge_kernel<DT, G>, p.merge_grid, 128, 0, s, p);
+    return launch_pdl(apex_merge_kernel<DT, G>, p.merge_grid, kMergeThreads, 0, s, p);
 }
 
 }  // namespace
+
+#ifdef APEX_TRACE
+extern "C" int apex_debug_trace(unsigned long long *host, int n) {
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpyFromSymbol(host, g_apex_trace, sizeof(unsigned long long) * 16 * (size_t)n);
+}
+extern "C" int apex_debug_trace_clear(void) {
+    static unsigned long long zero[1024][16];
+    return (int)cudaMemcpyToSymbol(g_apex_trace, zero, sizeof zero);
+}
+#endif
 
 bool decode_supported(apex_dtype dt, int group) {
     if (dt == APEX_F32) return group == 1;

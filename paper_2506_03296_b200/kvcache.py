@@ -136,6 +136,14 @@ class PagedKVCache:
     def set_grid(self, ctas: int):
         A.apex_kv_set_grid(self.handle, ctas)
 
+    def plan_ranges(self):
+        return A.apex_kv_plan_ranges(self.handle)
+
+    def set_sched(self, dyn_permille: int):
+        """-1: dynamic longest-first split items; 0..1000: stream-K static ranges with
+        that permille of the tiles left to the dynamic queue (bandwidth regime)."""
+        A.apex_kv_set_sched(self.handle, dyn_permille)
+
     def num_free_blocks(self) -> int:
         return A.apex_kv_num_free_blocks(self.handle)
 

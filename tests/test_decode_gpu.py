@@ -16,7 +16,13 @@ COMBOS = [("f32", 4, 4), ("f16", 4, 4), ("f16", 8, 2), ("f16", 16, 4), ("f16", 1
 RAGGED = [1, 2, 15, 16, 17, 31, 64, 100, 257, 1000, 2049]
 
 
-def run_case(dtype, hq, hkv, ctx, qamp=1.0, split=None, interleave=0, seed=0, num_blocks=None, poison=False):
+def torch_sm_count():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
+
+
+def run_case(dtype, hq, hkv, ctx, qamp=1.0, split=None, interleave=0, seed=0, num_blocks=None, poison=False,
+             sched=None, grid=None):
     import torch
     B = len(ctx)
     mbps = max(-(-c // 16) for c in ctx) + 1
@@ -27,6 +33,10 @@ def run_case(dtype, hq, hkv, ctx, qamp=1.0, split=None, interleave=0, seed=0, nu
             t.view(torch.uint8).fill_(0xFF)        # NaN bit patterns in every dtype
     if split is not None:
         cache.set_split(split)
+    if sched is not None:
+        cache.set_sched(sched)
+    if grid is not None:
+        cache.set_grid(grid)
     seqs = list(range(2, 2 + B))
     prefill(cache, seqs, ctx, seed=seed, interleave=interleave)
     out = decode_step(cache, seqs, ctx, seed=seed, qamp=qamp)
@@ -193,6 +203,24 @@ def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
     rows = list(range(0, batch * hq, max(1, batch * hq // 64)))
     ref = oracle_rows(seqs, [ctx] * batch, hq, hkv, dtype, rows=rows)
     check_close(to_f64(out, dtype).reshape(-1, 128)[rows], ref, dtype)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv", [("bf16", 32, 8), ("f16", 32, 32), ("f32", 8, 8), ("f16", 16, 2)])
+@pytest.mark.parametrize("sched", [-1, 0, 1, 100, 1000])
+@pytest.mark.parametrize("grid", [7, 0])
+def test_streamk_schedules(cuda_lib, dtype, hq, hkv, sched, grid):
+    """Stream-K static ranges (+ queue tail) in the bandwidth regime: ragged pairs
+    cut at CTA range boundaries are merged like split pairs; parity vs the oracle."""
+    ctx = [1000, 3000, 17, 5000, 1, 2500, 4097] if grid == 7 else [20000, 1, 33, 9000, 16000, 12000, 7000, 30001]
+    cache, seqs, out = run_case(dtype, hq, hkv, ctx, sched=sched, grid=grid or None, interleave=37, seed=3)
+    P = len(cache.plan_ranges()) - 1
+    assert P == (7 if grid == 7 else 2 * torch_sm_count())
+    T = sum(-(-c // 16) for c in ctx) * hkv
+    assert cache.decode_launches() == (2 if T > 64 * P else 1)   # bandwidth regime (+ merge kernel)
+    rows = None if grid == 7 else list(range(0, len(ctx) * hq, 3))
+    ref = oracle_rows(seqs, ctx, hq, hkv, dtype, seed=3, rows=rows)
+    got = out.reshape(-1, 128)[rows] if rows is not None else out
+    check_close(got, ref, dtype)
 
 
 def test_randomized_shapes_and_splits(cuda_lib):

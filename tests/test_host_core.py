@@ -136,8 +136,11 @@ def _check_plan(c, lens, hkv, bs=16):
         assert slots == list(range(slots[0], slots[0] + len(slots))) and len(slots) >= 2
         all_slots += slots
     assert len(all_slots) == len(set(all_slots)) and n_merges == len(parts)
-    # longest-first order
-    assert all(items[i][3] >= items[i + 1][3] for i in range(len(items) - 1))
+    # static per-CTA ranges, then the queue part in longest-first order
+    cb = c.plan_ranges()
+    assert cb[0] == 0 and all(cb[i] <= cb[i + 1] for i in range(len(cb) - 1)) and cb[-1] <= len(items)
+    dyn = items[cb[-1]:]
+    assert all(dyn[i][3] >= dyn[i + 1][3] for i in range(len(dyn) - 1))
     return items, n_merges
 
 
@@ -148,12 +151,52 @@ def test_planner_coverage_random():
         c = host_cache(num_q_heads=hkv * rnd.choice([1, 4]) if hkv != 8 else 32, num_kv_heads=hkv,
                        num_blocks=4096, max_blocks_per_seq=512, dtype="f16", max_new_tokens=1 << 16)
         c.set_grid(rnd.choice([0, 1, 7, 296]))
+        c.set_sched(rnd.choice([-1, -2, 0, 100]))
         if rnd.random() < 0.5:
             c.set_split(16 * rnd.choice([1, 2, 5, 64]))
         B = rnd.randint(1, 8)
         lens = [rnd.randint(1, 2000) for _ in range(B)]
         c.alloc(list(range(B)), lens)
         _check_plan(c, lens, hkv)
+
+
+def test_planner_streamk_ranges():
+    """Stream-K schedule: every tile covered once; CTA c's static range holds exactly
+    its quota of the first (1000 - dyn_permille) permille of the tiles, taken in
+    (row, kv head, block) order; the rest are queue items of bounded count."""
+    rnd = random.Random(7)
+    for trial in range(40):
+        hkv = rnd.choice([1, 2, 8])
+        c = host_cache(num_q_heads=hkv * (4 if hkv != 8 else 4), num_kv_heads=hkv, num_blocks=1 << 16,
+                       max_blocks_per_seq=2048, max_seqs=64, max_batch=64, dtype="bf16", max_new_tokens=1 << 20)
+        P = rnd.choice([1, 3, 7, 16])
+        perm = rnd.choice([0, 1, 50, 100, 333, 1000])
+        c.set_grid(P)
+        c.set_sched(perm)
+        B = rnd.randint(1, 40)
+        lens = [rnd.randint(1, 20000) for _ in range(B)]
+        c.alloc(list(range(B)), lens)
+        T = sum(-(-L // 16) for L in lens) * hkv
+        items, nm = _check_plan(c, lens, hkv)
+        cb = c.plan_ranges()
+        assert len(cb) == P + 1
+        if T <= 64 * P:
+            continue                                   # latency regime: one item per CTA, no stream-K
+        t_st = T - T * perm // 1000
+        flat = [(b, g, j) for b, L in enumerate(lens) for g in range(hkv) for j in range(-(-L // 16))]
+        pos = 0
+        for cta in range(P):
+            quota = t_st // P + (1 if cta < t_st % P else 0)
+            tiles = []
+            for (b, g, blk0, nblk, part, seq) in items[cb[cta]:cb[cta + 1]]:
+                tiles += [(b, g, j) for j in range(blk0, blk0 + nblk)]
+            assert tiles == flat[pos:pos + quota]       # contiguous, in flattened order, exact quota
+            pos += quota
+        assert len(items) - cb[-1] <= 8 * P + B * hkv   # bounded queue items
+    with pytest.raises(A.ApexError):
+        c.set_sched(1001)
+    with pytest.raises(A.ApexError):
+        c.set_sched(-3)
 
 
 def test_planner_split_chunk_and_auto():

@@ -1,0 +1,6 @@
+set -u
+O=gpurun_out/ab4; mkdir -p $O
+for c in c3 c5; do
+for r in 1 2; do for lib in v1 v2 v1sw2 v2sw2 v1sw1 v2sw1; do
+APEX_LIB=ab/$lib.so timeout 600 python tools/tune.py --config $c --chunks 0 --reps 10 --scheds=-2,-1 | grep '^{"grid' | sed "s/^/$lib /" >> $O/tune_$c.log
+done; done; done

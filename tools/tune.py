@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--chunks", default="0,256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--scheds", default="", help="comma list of apex_kv_set_sched values (-1 dynamic, "
+                                                 "0..1000 stream-K dynamic permille); empty = library default")
     a = ap.parse_args()
     w = WORKLOADS[a.config]
     ctx = [int(c) for c in w.contexts()]
@@ -40,10 +42,18 @@ def main():
     es = 4 if w.dtype == "f32" else 2
     nbytes = sum(c * w.num_kv_heads * 128 * 2 * es for c in ctx) + 2 * B * w.num_q_heads * 128 * es
     res = []
-    for grid in [int(x) for x in a.grids.split(",")]:
-        for chunk in [int(x) for x in a.chunks.split(",")]:
+    # a sched entry "-2:8/800/900/950" sets APEX_GUIDED for the guided planner
+    scheds = a.scheds.split(",") if a.scheds else [None]
+    for grid, chunk, sched in [(g, c, s) for g in [int(x) for x in a.grids.split(",")]
+                               for c in [int(x) for x in a.chunks.split(",")] for s in scheds]:
+        if True:
             cache.set_grid(grid)
             cache.set_split(chunk)
+            if sched is not None:
+                sv, _, gp = sched.partition(":")
+                if gp:
+                    os.environ["APEX_GUIDED"] = gp.replace("/", ",")
+                cache.set_sched(int(sv))
             try:
                 cache.alloc(seqs, [0] * B)
             except Exception as e:          # chunk too small for the workspace
@@ -63,7 +73,7 @@ def main():
                 ts.append(e0.elapsed_time(e1) * 1e3)
             items, merges = cache.plan()
             med = statistics.median(ts)
-            r = dict(grid=grid, chunk=chunk, items=len(items), merges=merges, us_med=med, us_min=min(ts),
+            r = dict(grid=grid, chunk=chunk, sched=sched, items=len(items), merges=merges, us_med=med, us_min=min(ts),
                      gbs=nbytes / med / 1e3)
             res.append(r)
             print(json.dumps(r), flush=True)
