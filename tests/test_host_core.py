@@ -264,12 +264,28 @@ def test_planner_choice_at_config_scale():
     c5.alloc(list(range(1024)), [1] * 1024)
     dt = time.perf_counter() - t0
     items, nm = c5.plan()
-    assert len(items) == 8192 and nm == 0
+    # guided (default): chunk T/(8P) = 3547 blocks > 1025, so the first 90% of the pairs
+    # (flattened order) stay whole; only the last 5% / 2% are cut (in 2 / 3 pieces)
+    whole = {(it[0], it[1]) for it in items if it[4] < 0}
+    assert len(whole) == 8192 - nm and nm <= 0.1 * 8192 and nm > 0
+    assert all((b, g) in whole for b in range(1024) for g in range(8) if b * 8 + g < 0.9 * 8192)
     assert dt < 0.05                                 # per-step host planning stays cheap
+    c5.set_sched(-1)                                 # uniform dynamic split: ceil(T/16P) = 1774 > 1025 -> no split
+    c5.alloc(list(range(1024)), [1] * 1024)
+    items, nm = c5.plan()
+    assert len(items) == 8192 and nm == 0
     # C3-like: 1024 pairs of 512 blocks (3.5 per CTA) -> split
     c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=128 * 513, max_seqs=128, max_blocks_per_seq=520,
                     max_batch=128, max_new_tokens=1 << 21)
     c3.set_grid(296)
     c3.alloc(list(range(128)), [8192] * 128)
     items, nm = _check_plan(c3, [8192] * 128, 8)
+    # guided: chunk ceil(T/8P) = 222 blocks -> 3 pieces of 171; the last 10 / 5 / 2% of the
+    # pairs use chunks 111 / 55 / 27 -> 5 / 10 / 19 pieces, run last (longest first)
+    sizes = sorted({it[3] for it in items})
+    assert nm == 1024 and max(sizes) == 171 and min(sizes) <= 27
+    assert items[0][3] == 171 and items[-1][3] == min(sizes)
+    c3.set_sched(-1)
+    c3.alloc(list(range(128)), [1] * 128)
+    items, nm = _check_plan(c3, [8193] * 128, 8)
     assert len(items) == 5 * 1024 and nm == 1024     # chunk ceil(T/16P) = 111 blocks -> 5 pieces
