@@ -63,6 +63,9 @@ namespace {
 #ifndef APEX_EARLY_RELEASE
 #define APEX_EARLY_RELEASE 0
 #endif
+#ifndef APEX_MERGE_UNROLL
+#define APEX_MERGE_UNROLL 16
+#endif
 #ifndef APEX_MAX_SLOTS
 #define APEX_MAX_SLOTS 24
 #endif
@@ -73,6 +76,7 @@ constexpr int NC = APEX_NC;              // consumer warps
 constexpr int NTHREADS = 32 * (NC + 1);   // producer warp + NC consumer warps
 constexpr int IR = 4;                    // item-ring entries
 constexpr int CTAS_PER_SM = APEX_CTAS_PER_SM;
+constexpr int kMergeUnroll = APEX_MERGE_UNROLL;   // parts in flight per thread in the LSE merge
 constexpr int kTileRows = kBlock;        // 16 tokens per tile
 // smem tile of one (block, kv head): [segment][32 rows: K 0-15, V 16-31][128 B], 128-B swizzled
 constexpr int kSegStride = 2 * kTileRows * 128;
@@ -90,14 +94,15 @@ template <int DT, int G> struct Cfg {
     static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of the K (or the V) half of a tile
     static constexpr int CB_O = NC * G * kHeadDim * 4;       // per-warp O for the item merge
     static constexpr int CB_ML = NC * G * 2 * 4 + 16;     // + merge flag
+    static constexpr int MSCR = NC * 32 * (16 + 8);        // fused merge: red (float4) + redml (float2) per thread
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
-    static constexpr int FIXED = CB_O + CB_ML + RING + 2 * IR * 8 + 1024;
+    static constexpr int FIXED = CB_O + CB_ML + NC * 32 * 24 + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
     static constexpr int SW = (S0 > APEX_MAX_SLOTS ? APEX_MAX_SLOTS : S0) / NC;   // slots per consumer warp
     static constexpr int STAGES = SW * NC;
     static constexpr int TILES = STAGES * 2 * TILE;
     static constexpr int BARS = (2 * STAGES + 2 * IR) * 8;
-    static constexpr int TOTAL = TILES + BARS + RING + CB_O + CB_ML + 1024;   // + alignment slack
+    static constexpr int TOTAL = TILES + BARS + RING + CB_O + CB_ML + MSCR + 1024;   // + alignment slack
     static_assert(TOTAL <= kSmemPerCta, "shared memory budget");
     static_assert(SW >= 1, "ring too shallow");
 };
@@ -504,36 +509,58 @@ template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
 // M = max m_i, out = sum 2^(m_i-M) O_i / sum 2^(m_i-M) l_i.  Partials written by
 // other CTAs are read through L2 (ld.global.cg).
 //
-// Parallel form (nparts * G * 2 + 2 G floats of scratch `sm` available): the
-// pair's (m, l) are contiguous (consecutive partial slots), so all threads load
-// them in ONE round trip into smem; per-row max and weights w_i = 2^(m_i - M)
-// are formed there; then thread (output float4 o, part group gr) accumulates
-// w_i O_i over parts i = gr, gr + ngr, ... (independent loads, many in flight),
-// and part groups are summed through smem in fixed order.  This replaces a
-// per-thread serial loop whose dependent batches of loads made a 37-way merge
-// cost ~7 us and a 256-way merge ~150 us.  `sync` is a barrier over the nt
-// participating threads; `red` (ngr > 1 only) holds ngr * G * 32 float4.
+// One pass with a running max: thread (output float4 o, part group gr) folds
+// parts i = gr, gr + ngr, ... into (M, den, acc) with acc <- acc 2^(M-M') +
+// 2^(m_i-M') O_i.  The loads of all parts are independent of the running state,
+// so an unrolled loop keeps 16 parts in flight per thread (a 37-way merge is
+// ~3 round trips; the former max-then-sum form needed a dependent second pass).
+// Part groups (ngr > 1, separate merge kernel: 256 threads) are combined
+// through `red`/`redml` in fixed group order.  `sync` is a barrier over the nt
+// participating threads.
 template <int DT, int G, typename Sync>
-__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt, float *sm,
-                                           int sm_cap, float4 *red, int red_cap, Sync sync) {
-    const int np = mg.nparts, nml = np * G;
+__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt, float4 *red,
+                                           float2 *redml, int red_cap, Sync sync) {
+    const int np = mg.nparts;
     constexpr int NOUT = G * kHeadDim / 4;                    // float4 outputs of the pair
     const float2 *ml = reinterpret_cast<const float2 *>(p.part_ml) + (size_t)mg.part0 * G;
-    if (2 * nml + 2 * G > sm_cap) {
-        // too many parts for the scratch: serial form
-        for (int idx = t; idx < NOUT; idx += nt) {
-            const int row = idx / (kHeadDim / 4), d4 = (idx % (kHeadDim / 4)) * 4;
+    const int ngr = red ? max(1, min(nt, red_cap) / NOUT) : 1;   // part groups (1 when NOUT >= nt)
+    for (int idx = t; idx < NOUT * ngr; idx += nt) {
+        const int o = idx % NOUT, gr = idx / NOUT;
+        const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
+        const float *po = p.part_o + ((size_t)mg.part0 * G + row) * kHeadDim + d4;
+        float M = -INFINITY, den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+#pragma unroll kMergeUnroll
+        for (int i = gr; i < np; i += ngr) {
+            const float2 mi = __ldcg(ml + (size_t)i * G + row);
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + (size_t)i * G * kHeadDim));
+            const float Mn = fmaxf(M, mi.x);
+            const float al = ex2_diff(M, Mn), e = ex2_diff(mi.x, Mn);
+            den = fmaf(den, al, e * mi.y);
+            a = fmaf(a, al, e * v.x);
+            b = fmaf(b, al, e * v.y);
+            c = fmaf(c, al, e * v.z);
+            d = fmaf(d, al, e * v.w);
+            M = Mn;
+        }
+        if (ngr == 1) {
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
+        } else {
+            red[gr * NOUT + o] = make_float4(a, b, c, d);
+            redml[gr * NOUT + o] = make_float2(M, den);
+        }
+    }
+    if (ngr > 1) {
+        sync();
+        for (int o = t; o < NOUT; o += nt) {
+            const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
             float M = -INFINITY;
-#pragma unroll 8
-            for (int i = 0; i < np; ++i) M = fmaxf(M, __ldcg(ml + (size_t)i * G + row).x);
+            for (int gr = 0; gr < ngr; ++gr) M = fmaxf(M, redml[gr * NOUT + o].x);
             float den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
-#pragma unroll 8
-            for (int i = 0; i < np; ++i) {
-                const size_t pi = (size_t)(mg.part0 + i) * G + row;
-                const float2 v2 = __ldcg(ml + (size_t)i * G + row);
-                const float e = ex2_diff(v2.x, M);
-                const float4 v = __ldcg(reinterpret_cast<const float4 *>(p.part_o + pi * kHeadDim + d4));
-                den = fmaf(e, v2.y, den);
+            for (int gr = 0; gr < ngr; ++gr) {
+                const float2 mlg = redml[gr * NOUT + o];
+                const float e = ex2_diff(mlg.x, M);
+                const float4 v = red[gr * NOUT + o];
+                den = fmaf(e, mlg.y, den);
                 a = fmaf(e, v.x, a);
                 b = fmaf(e, v.y, b);
                 c = fmaf(e, v.z, c);
@@ -541,78 +568,8 @@ __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeIte
             }
             store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
         }
-        return;
+        sync();                                                // red reusable for the next pair
     }
-    float *sw = sm, *sl = sm + nml, *sM = sm + 2 * nml, *sden = sM + G;
-    if (t == 0 && !red) TRACE(12);
-    for (int i = t; i < nml; i += nt) {
-        const float2 v = __ldcg(ml + i);
-        sw[i] = v.x;
-        sl[i] = v.y;
-    }
-    sync();
-    if (t == 0 && !red) TRACE(13);
-    const int lane = t & 31, wid = t >> 5, nw = nt >> 5;
-    for (int row = wid; row < G; row += nw) {                 // per-row max, then weights and denominator
-        float M = -INFINITY;
-        for (int i = lane; i < np; i += 32) M = fmaxf(M, sw[i * G + row]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        float den = 0.f;
-        for (int i = lane; i < np; i += 32) {
-            const float e = ex2_diff(sw[i * G + row], M);
-            sw[i * G + row] = e;
-            den = fmaf(e, sl[i * G + row], den);
-        }
-        // fixed-order sum: lane partials combined by a fixed butterfly (deterministic)
-#pragma unroll
-        for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-        if (lane == 0) {
-            sM[row] = M;
-            sden[row] = den;
-        }
-    }
-    sync();
-    if (t == 0 && !red) TRACE(14);
-    const int ngr = red ? min(max(1, nt / NOUT), red_cap / NOUT) : 1;
-    for (int idx = t; idx < NOUT * ngr; idx += nt) {
-        const int o = idx % NOUT, gr = idx / NOUT;
-        const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
-        float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
-        const float *po = p.part_o + ((size_t)mg.part0 * G + row) * kHeadDim + d4;
-#pragma unroll 16
-        for (int i = gr; i < np; i += ngr) {
-            const float e = sw[i * G + row];
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + (size_t)i * G * kHeadDim));
-            a = fmaf(e, v.x, a);
-            b = fmaf(e, v.y, b);
-            c = fmaf(e, v.z, c);
-            d = fmaf(e, v.w, d);
-        }
-        if (ngr == 1) {
-            const float den = sden[row];
-            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
-        } else {
-            red[gr * NOUT + o] = make_float4(a, b, c, d);
-        }
-    }
-    if (ngr > 1) {
-        sync();
-        for (int o = t; o < NOUT; o += nt) {
-            const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
-            float4 acc = red[o];
-            for (int gr = 1; gr < ngr; ++gr) {
-                const float4 v = red[gr * NOUT + o];
-                acc.x += v.x;
-                acc.y += v.y;
-                acc.z += v.z;
-                acc.w += v.w;
-            }
-            const float den = sden[row];
-            store_out<DT>(p, mg.b, mg.g * G + row, d4, acc.x / den, acc.y / den, acc.z / den, acc.w / den);
-        }
-    }
-    sync();                                                    // scratch reusable by the caller
 }
 
 // ------------------------------------------------------------------ decode kernel
@@ -631,6 +588,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     float *cb_m = cb_o + NC * G * kHeadDim;
     float *cb_l = cb_m + NC * G;
     volatile int *merge_flag = reinterpret_cast<volatile int *>(cb_l + NC * G);
+    float4 *mred = reinterpret_cast<float4 *>(smem + S::TILES + S::BARS + S::RING + S::CB_O + S::CB_ML);
+    float2 *mredml = reinterpret_cast<float2 *>(mred + NC * 32);
     const uint32_t tiles_u = smem_u32(smem);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES;
     const uint32_t ifull0 = empty0 + 8 * STAGES, iempty0 = ifull0 + 8 * IR;
@@ -666,6 +625,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         const int n_items = p.hdr->n_items;    // this step's work-list length (device header)
         int s_next = __ldg(p.cta_begin + blockIdx.x);
         const int s_end = __ldg(p.cta_begin + blockIdx.x + 1), q_base = __ldg(p.cta_begin + gridDim.x);
+        // speculative load of item blockIdx.x (the first item of CTA i is item i unless the
+        // plan has stream-K ranges): issued together with the header loads, one round
+        // trip earlier than a load that waits for cta_begin (the list has >= grid slots)
+        const WorkItem spec = p.items[blockIdx.x];
         int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
 #pragma unroll
         for (int q = 0; q < NC; ++q) pc[q] = 0;
@@ -687,7 +650,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
-            const WorkItem it = p.items[idx];
+            const WorkItem it = (k == 0 && idx == (int)blockIdx.x) ? spec : p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 mbar_arrive(ifull0 + 8 * slot);
@@ -801,13 +764,21 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             if (k == 0 && threadIdx.x == 32) TRACE(8);
 #endif
             if (FUSE && it.part >= 0) {
-                // last-arriving split of this (b, g) pair merges all its partials (fused LSE merge)
-                __threadfence();
+                // last-arriving split of this (b, g) pair merges all its partials (fused LSE
+                // merge).  Release/acquire through one thread (CUTLASS-semaphore pattern):
+                // bar.sync orders the CTA's partial stores before thread 32's gpu-scope
+                // acq_rel fence + counter atomic; the last arriver's fence + bar.sync order
+                // the other CTAs' partials before every thread's loads (no per-thread
+                // sequentially consistent __threadfence).
                 named_bar_sync(1, NC * 32);
                 if (threadIdx.x == 32) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     const int done = atomicAdd(p.merge_counters + it.mg, 1);
                     const int last = done == p.merges[it.mg].nparts - 1;
-                    if (last) p.merge_counters[it.mg] = 0;      // every split has arrived: re-arm
+                    if (last) {
+                        p.merge_counters[it.mg] = 0;            // every split has arrived: re-arm
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    }
                     *merge_flag = last;
                 }
                 named_bar_sync(1, NC * 32);
@@ -815,10 +786,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 if (k == 0 && threadIdx.x == 32) TRACE(9);
 #endif
                 if (*merge_flag) {
-                    __threadfence();
-                    // scratch: the per-warp O buffer (free after this item's warp merge)
-                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32, cb_o, NC * G * kHeadDim,
-                                      nullptr, 0, [] { named_bar_sync(1, NC * 32); });
+                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
+                                      [] { named_bar_sync(1, NC * 32); });
 #ifdef APEX_TRACE
                     named_bar_sync(1, NC * 32);
                     if (threadIdx.x == 32) TRACE(10);
@@ -833,16 +802,15 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 
 // log-sum-exp merge of split pairs as its own launch (bandwidth regime): one CTA
 // per (b, g) pair, so merging never stalls a decode CTA's TMA stream.
-constexpr int kMergeThreads = 256;
-constexpr int kMergeScratch = 6144;                        // floats: (m, l) of up to 3072 / G parts
+constexpr int kMergeThreads = 512;
 template <int DT, int G>
 __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeParams p) {
-    __shared__ float sm[kMergeScratch];
-    __shared__ float4 red[kMergeThreads];                   // part-group partial sums (G * 32 * ngr float4)
+    __shared__ float4 red[kMergeThreads];                   // part-group partials (G * 32 * ngr)
+    __shared__ float2 redml[kMergeThreads];
     asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
     const int n = p.hdr->n_merges;                          // fixed grid, grid-stride over this step's pairs
     for (int i = blockIdx.x; i < n; i += gridDim.x)
-        merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x, sm, kMergeScratch, red, kMergeThreads,
+        merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x, red, redml, kMergeThreads,
                           [] { __syncthreads(); });
 }
 

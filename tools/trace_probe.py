@@ -26,6 +26,7 @@ def main():
     from paper_2506_03296_b200 import apex as A
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="bf16,32,8,1,16384")
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between calls")
     a = ap.parse_args()
     d, *n = a.shape.split(",")
     dtype, (hq, hkv, batch, ctx) = d, [int(x) for x in n]
@@ -42,7 +43,8 @@ def main():
     q = gen_dev(cache, 0, 0, seqs, [ctx] * batch, hq)
     out = torch.empty_like(q)
     for r in range(4):
-        flush.fill_(r)
+        if not a.no_flush:
+            flush.fill_(r)
         L.apex_debug_trace_clear()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
