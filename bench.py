@@ -6,7 +6,9 @@
 
 A step is one pass of the whole hot path over one batch:
 apex_kv_alloc (+1 token per request; planner + metadata upload) and, for each of
-the L logical layers, apex_kv_append + apex_decode_attention (+ the LSE merge).
+the L logical layers, the KV append + decode attention (+ the LSE merge) -- by
+default in one launch (apex_decode_attention_append; --append separate runs
+apex_kv_append + apex_decode_attention).
 value = decode tokens/s of the whole job (one token per request per step needs
 all L layers) = sum_ranks(B_r) * K / max_ranks(time of K steps).
 
@@ -64,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--append", choices=["fused", "separate"], default="fused",
+                    help="fused: apex_decode_attention_append (append inside the decode launch); "
+                         "separate: apex_kv_append + apex_decode_attention")
     ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
                     help="head mode: NCCL all_gather_into_tensor, or stores into peers' symmetric memory "
                          "from the decode epilogue (experimental, needs >= 2 GPUs)")
@@ -353,6 +358,7 @@ def run_apex(args):
     gathered = [None] * P
     head_mode = w.name == "c5" and args.mode == "head" and world > 1
     fused = head_mode and args.gather == "fused"
+    fused_append = args.append == "fused" and not fused      # the symmetric-memory epilogue uses the _ex call
     if head_mode:
         from paper_2506_03296_b200.sharding import gather_heads
     if fused:
@@ -375,10 +381,13 @@ def run_apex(args):
         cache.alloc(seq, ones)
         for l in range(L):
             p = l % P
-            cache.append(p, ks[p], vs[p])
+            if not fused_append:
+                cache.append(p, ks[p], vs[p])
             if timed_idx is not None:
                 ev[timed_idx * L + l][0].record()
-            if fused:
+            if fused_append:
+                cache.decode_append(p, qs[p], ks[p], vs[p], out=outs[p])
+            elif fused:
                 buf, hdl = symm[p]
                 A.apex_decode_attention_ex(cache.handle, p, qs[p].data_ptr(), list(hdl.buffer_ptrs),
                                            w.num_q_heads * D, wl["q_off"], 1.0 / D ** 0.5,
@@ -461,7 +470,9 @@ def run_apex(args):
                                 f"flushed: {step_kv_bytes / 2**20:.1f} MiB of KV per step fits the "
                                 f"{l2_bytes / 2**20:.0f} MiB L2, so a 512 MiB buffer is written before every "
                                 "step (outside the per-step events; time = sum of per-step intervals)"),
-                         "work_items_per_layer": n_items, "split_merges_per_layer": n_merges},
+                         "work_items_per_layer": n_items, "split_merges_per_layer": n_merges,
+                         "append": "fused into the decode launch (apex_decode_attention_append)" if fused_append
+                                   else "separate apex_kv_append launch"},
               "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,
               "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                            "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.config),
@@ -470,7 +481,7 @@ def run_apex(args):
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
-              "gpu_launches": K * (1 + L * (1 + decode_launches)),   # deltas + L x (append, decode[, merge])
+              "gpu_launches": K * (1 + L * ((0 if fused_append else 1) + decode_launches)),   # deltas + L x ([append,] decode[, merge])
               "prefill_s": t_fill}
     if clk:
         result["clocks"] = clk
@@ -547,8 +558,11 @@ def run_apex(args):
                     vd[j].copy_(vh[p], non_blocking=True)
                     h2d_done[j].record(h2d_s)
                 comp.wait_event(h2d_done[j])
-                cache.append(p, kd[j], vd[j])
-                cache.decode(p, qd[j], out=od[j])
+                if fused_append:
+                    cache.decode_append(p, qd[j], kd[j], vd[j], out=od[j])
+                else:
+                    cache.append(p, kd[j], vd[j])
+                    cache.decode(p, qd[j], out=od[j])
                 if head_mode:
                     oh[p] = gather_heads(od[j] if not gloo else od[j].cpu()).cpu()
                     buf_free[j].record(comp)

@@ -152,6 +152,18 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
                                      int64_t out_row_stride, int32_t out_head_offset, float scale,
                                      apex_stream stream);
 
+/* apex_kv_append + apex_decode_attention in ONE launch for
+   a pure decode step: every sequence of the last apex_kv_alloc has exactly one
+   new token (else APEX_EINVAL, nothing enqueued).  k_new / v_new: device
+   [batch][Hkv][D] in the step's row order, 16-byte aligned.  The CTA that
+   streams a sequence's last block writes the new K/V row into the pool (so
+   later steps see it, exactly as apex_kv_append would) and patches it into its
+   shared-memory copy of the tile before use; outputs and pools are
+   bit-identical to the two-call sequence.  Other arguments as
+   apex_decode_attention. */
+apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void *q, const void *k_new,
+                                         const void *v_new, void *out, float scale, apex_stream stream);
+
 /* ---- planner knobs and introspection (host state only; no CUDA calls) ---- */
 
 /* Split-KV chunk in tokens (multiple of 16) used by the NEXT apex_kv_alloc;

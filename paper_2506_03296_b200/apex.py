@@ -25,7 +25,8 @@ EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex
            "apex_kv_append", "apex_decode_attention", "apex_kv_set_split", "apex_kv_set_grid", "apex_kv_set_sched",
            "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan", "apex_kv_plan_ranges",
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
-           "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex"]
+           "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex",
+           "apex_decode_attention_append"]
 STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
 
 
@@ -96,6 +97,8 @@ def lib():
             "apex_kv_decode_launches": (c_int32, [c_void_p]),
             "apex_decode_attention_ex": (c_int, [c_void_p, c_int32, c_void_p, POINTER(c_void_p), c_int32, c_int64,
                                                  c_int32, c_float, c_void_p]),
+            "apex_decode_attention_append": (c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                                     c_float, c_void_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -149,6 +152,11 @@ def apex_kv_append(kv: int, layer: int, k_new_ptr: int, v_new_ptr: int, stream: 
 
 def apex_decode_attention(kv: int, layer: int, q_ptr: int, out_ptr: int, scale: float, stream: int = 0) -> None:
     _check(lib().apex_decode_attention(kv, int(layer), q_ptr, out_ptr, float(scale), stream))
+
+
+def apex_decode_attention_append(kv: int, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, out_ptr: int,
+                                 scale: float, stream: int = 0) -> None:
+    _check(lib().apex_decode_attention_append(kv, int(layer), q_ptr, k_ptr, v_ptr, out_ptr, float(scale), stream))
 
 
 def apex_kv_set_split(kv: int, chunk_tokens: int) -> None:

@@ -212,6 +212,7 @@ struct apex_kv {
 
     // the current step (defined by the last successful apex_kv_alloc)
     bool have_step = false;
+    bool single_token_step = false;   // every sequence of the step has n_new == 1 (fused append allowed)
     int32_t batch = 0, n_rows = 0;
     std::vector<int32_t> batch_seq, slots;
     std::vector<WorkItem> items;
@@ -612,6 +613,8 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     kv->batch = n;
     kv->n_rows = (int32_t)rows;
     kv->have_step = true;
+    kv->single_token_step = true;
+    for (int32_t i = 0; i < n; ++i) kv->single_token_step = kv->single_token_step && n_new[i] == 1;
     apex_status st = plan_step(kv, lens);
     if (st != APEX_OK) {
         kv->have_step = false;   // blocks stay allocated (state is consistent); the step is unusable
@@ -696,9 +699,11 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
                                     stream);
 }
 
-apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
-                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
-                                     apex_stream stream) {
+}  // extern "C"
+
+static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const void *k_new, const void *v_new,
+                               void *const *outs, int32_t n_out, int64_t out_row_stride, int32_t out_head_offset,
+                               float scale, apex_stream stream) {
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");
     if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
     if (!kv->have_step) return fail(APEX_EINVAL, "apex_decode_attention before apex_kv_alloc");
@@ -737,11 +742,39 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
     p.scale_log2 = (float)((double)scale * 1.4426950408889634);   // log2(e)
     p.tma_segs = kv->tma_segs;
     p.fuse_merge = kv->fuse_merge ? 1 : 0;
+    if (k_new) {
+        if (!v_new || (((uintptr_t)k_new | (uintptr_t)v_new) & 15))
+            return fail(APEX_EINVAL, "k_new/v_new NULL or not 16-byte aligned");
+        if (!kv->single_token_step)
+            return fail(APEX_EINVAL, "fused append needs exactly one new token per sequence in the step "
+                                     "(use apex_kv_append + apex_decode_attention)");
+        p.k_new = k_new;
+        p.v_new = v_new;
+        p.kv_pool = kv->kv_pools[layer];
+        p.num_blocks = kv->d.num_blocks;
+    }
     // fixed persistent grid (CTAs without an item exit at once): every launch parameter is
     // step-invariant, so the per-layer launches can be captured in a CUDA graph
     const int grid = kv->plan_grid;   // cta_begin has plan_grid + 1 entries
     cudaError_t e = apex::launch_decode(kv->d.dtype, kv->group, kv->tmaps[layer], p, grid, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_decode_attention");
+}
+
+extern "C" {
+
+apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
+                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
+                                     apex_stream stream) {
+    return decode_impl(kv, layer, q, nullptr, nullptr, outs, n_out, out_row_stride, out_head_offset, scale, stream);
+}
+
+apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void *q, const void *k_new,
+                                         const void *v_new, void *out, float scale, apex_stream stream) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (!k_new || !v_new) return fail(APEX_EINVAL, "k_new/v_new is NULL");
+    void *outs[1] = {out};
+    return decode_impl(kv, layer, q, k_new, v_new, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim, 0, scale,
+                       stream);
 }
 
 // ---------------------------------------------------------------- cost model

@@ -73,6 +73,14 @@ struct DecodeParams {
     float scale_log2;          // scale * log2(e)
     int32_t tma_segs;          // 1: one 3-D TMA op per tile; n: n 2-D ops (one per 128-B segment)
     int32_t fuse_merge;        // 1: last split per pair merges in-kernel; 0: apex_merge_kernel launch
+    // fused append (apex_decode_attention_append; every sequence of the step has
+    // exactly one new token, row b of k_new/v_new [B][Hkv][D]): the CTA that loads a
+    // sequence's last block writes the new K/V row into the pool (producer) and
+    // patches it into the shared-memory tile (consumer) before using it
+    const void *k_new;         // nullptr: no fused append
+    const void *v_new;
+    void *kv_pool;             // this layer's pool
+    int32_t num_blocks;
 };
 
 struct TmaMap {

@@ -237,6 +237,41 @@ __device__ __forceinline__ void store_out(const DecodeParams &p, int b, int head
     for (int i = 0; i < p.n_out; ++i) store4<DT>(p.out[i], o, a, bb, c, d);
 }
 
+// ------------------------------------------------------------------ fused append
+// The new token's K and V rows (row b of k_new / v_new, kv head g) as 16-byte
+// chunks: i in [0, 2*CPR): tensor i / CPR (0 = K, 1 = V), chunk cc = i % CPR of
+// the D-vector (segment cc / 8, 16-B column cc % 8 inside the 128-B segment).
+template <int ES> struct NewRow {
+    static constexpr int CPR = kHeadDim * ES / 16;   // 16-B chunks per D-vector
+    __device__ __forceinline__ static uint4 load(const DecodeParams &p, int b, int g, int i) {
+        const uint8_t *src = static_cast<const uint8_t *>(i < CPR ? p.k_new : p.v_new);
+        return __ldg(reinterpret_cast<const uint4 *>(src + ((size_t)b * p.num_kv_heads + g) * kHeadDim * ES) +
+                     (i % CPR));
+    }
+    // producer: the row into the pool (layout [blocks][Hkv][2][16][D])
+    __device__ __forceinline__ static void to_pool(const DecodeParams &p, int b, int g, int phys, int t, int lane) {
+        for (int i = lane; i < 2 * CPR; i += 32) {
+            uint8_t *dst = static_cast<uint8_t *>(p.kv_pool) +
+                           ((((size_t)phys * p.num_kv_heads + g) * 2 + i / CPR) * kTileRows + t) * kHeadDim * ES;
+            reinterpret_cast<uint4 *>(dst)[i % CPR] = load(p, b, g, i);
+        }
+    }
+    // consumer: the row into the 128-B-swizzled smem tile ([segment][32 rows][128 B])
+    // over whatever the bulk copy brought for it, before the tile is used
+    __device__ __forceinline__ static void to_tile(const DecodeParams &p, int b, int g, uint32_t kt, int t, int lane) {
+        for (int i = lane; i < 2 * CPR; i += 32) {
+            const uint4 v = load(p, b, g, i);
+            const int cc = i % CPR, sg = cc / 8, c = cc % 8, row = (i / CPR) * kTileRows + t;
+            const uint32_t a = kt + sg * kSegStride + row * 128 + ((c ^ (row & 7)) << 4);
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                         : "memory");
+        }
+        // generic-proxy writes to a slot the bulk-copy (async) proxy will refill later
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+    }
+};
+
 // ------------------------------------------------------------------ consumers
 // Running online-softmax state of one consumer warp for its share of an item.
 // MMA layout: row = lane/4 (q head of the group), 2 columns per n-tile.
@@ -668,6 +703,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 #endif
                 for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
+                    if (p.k_new && it.blk0 + j0 + jj == (it.len - 1) / kTileRows)   // fused append
+                        NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
                     const int w = (j0 + jj) % NC;
                     int m = 0;
 #pragma unroll
@@ -722,6 +759,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 #endif
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;
+                if (p.k_new && it.blk0 + j == (it.len - 1) / kTileRows)   // fused append: patch the new row
+                    NewRow<C::ES>::to_tile(p, it.b, it.g, kt, (it.len - 1) % kTileRows, lane);
                 st.tile(kt, kt + kVOff, valid, p.scale_log2, lane, [&] {
                     __syncwarp();                                 // every lane's smem reads of the slot are done
                     if (lane == 0) mbar_arrive(empty0 + 8 * s);   // release it to the producer

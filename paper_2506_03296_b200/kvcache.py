@@ -107,6 +107,24 @@ class PagedKVCache:
         A.apex_decode_attention(self.handle, layer, q.data_ptr(), out.data_ptr(), scale, self._stream())
         return out
 
+    def decode_append(self, layer: int, q, k_new, v_new, out=None, scale: float | None = None):
+        """append(layer, k_new, v_new) + decode(layer, q) in one launch (pure decode step:
+        one new token per sequence).  Bit-identical to the two calls."""
+        import torch
+        B = len(self.batch_seq_ids)
+        self._check_rows(q, B, self.num_q_heads)
+        self._check_rows(k_new, B, self.num_kv_heads)
+        self._check_rows(v_new, B, self.num_kv_heads)
+        if out is None:
+            out = torch.empty_like(q)
+        else:
+            self._check_rows(out, B, self.num_q_heads)
+        if scale is None:
+            scale = 1.0 / math.sqrt(self.head_dim)
+        A.apex_decode_attention_append(self.handle, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                                       out.data_ptr(), scale, self._stream())
+        return out
+
     def decode_into(self, layer: int, q, outs, head_offset: int = 0, scale: float | None = None):
         """Decode writing this handle's q heads into each full-width [B][H_total][D] tensor of
         `outs` at head `head_offset` (fused all-gather epilogue when `outs` are peer-mapped

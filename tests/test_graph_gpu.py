@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("dtype,hq,hkv,ctx", [("bf16", 32, 8, [5, 700, 2000, 31]), ("f16", 8, 8, [100, 3000]),
                                               ("f32", 4, 4, [15, 64, 999]),
                                               ("bf16", 32, 8, [8192] * 16)])   # bandwidth regime + merges
-def test_graph_replay_matches_eager_and_oracle(cuda_lib, dtype, hq, hkv, ctx):
+@pytest.mark.parametrize("fused_append", [False, True])
+def test_graph_replay_matches_eager_and_oracle(cuda_lib, dtype, hq, hkv, ctx, fused_append):
     import torch
     B = len(ctx)
     steps = 18                                          # crosses a 16-token block boundary
@@ -51,8 +52,11 @@ def test_graph_replay_matches_eager_and_oracle(cuda_lib, dtype, hq, hkv, ctx):
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):
                 with torch.cuda.graph(graph, stream=stream):
-                    graph_c.append(0, k_buf, v_buf)
-                    graph_c.decode(0, q_buf, out=out_buf)
+                    if fused_append:
+                        graph_c.decode_append(0, q_buf, k_buf, v_buf, out=out_buf)
+                    else:
+                        graph_c.append(0, k_buf, v_buf)
+                        graph_c.decode(0, q_buf, out=out_buf)
             torch.cuda.current_stream().wait_stream(stream)
         graph.replay()
         eager_c.append(0, k_buf, v_buf)
