@@ -34,6 +34,8 @@
 //  * every launch parameter is step-invariant (counts from the device step
 //    header, fixed grids), so the launches are CUDA-graph capturable, and they
 //    use programmatic dependent launch (griddepcontrol) to overlap prologues.
+#include <type_traits>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -537,7 +539,152 @@ template <int DT> struct SimtConsumer {
     }
 };
 
-template <int DT, int G> struct ConsumerSel { using T = MmaConsumer<DT, G>; };
+// Transposed tensor-core consumer for GQA (g >= 2, 16-bit): the q-group is the
+// N = 8 side of mma.m16n8k16 instead of padded M = 16 rows, so a 16-token tile
+// costs 16 HMMA instead of 48 and the O accumulators halve (32 floats/thread):
+//   S^T (16 tok x 8 heads) = K (16 tok x 16 d, A, ldmatrix) * Q^T (B, registers), 8 k-steps
+//   O^T (128 d x 8 heads) += V^T (A: ldmatrix.trans of the V rows) * P^T (B)
+// P^T's B fragments come from the S^T accumulators by movmatrix.trans (two 8x8
+// b16 transposes), the per-head softmax statistics reduce over the 8 lanes
+// holding one head column.  Heads >= G have zero q (finite, ignored).
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
+}
+template <int DT>
+__device__ __forceinline__ void mma_16816_full(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    if constexpr (DT == APEX_BF16)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int DT, int G> struct MmaConsumerT {
+    uint32_t qb[8][2];          // B fragments of Q^T per k-step: q[h = lane/4][d pairs], zero for h >= G
+    float o[8][4];              // O^T accumulators, m-tile md covers dims md*16 .. md*16+15
+    float m[2], l[2];           // per head column (lane%4)*2 + j: running max (log2) and partial sum
+
+    __device__ __forceinline__ void begin(const uint8_t *qg, const DecodeParams &, int lane) {
+        const int h = lane >> 2, tid = lane & 3;
+        const uint32_t *qrow = reinterpret_cast<const uint32_t *>(qg + (size_t)h * kHeadDim * 2);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qb[kk][0] = h < G ? qrow[kk * 8 + tid] : 0u;
+            qb[kk][1] = h < G ? qrow[kk * 8 + 4 + tid] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+        m[0] = m[1] = -INFINITY;
+        l[0] = l[1] = 0.f;
+    }
+
+    template <typename Release>
+    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float scale_log2, int lane,
+                                         Release release) {
+        const int tid = lane & 3, t8 = lane >> 2;
+        // ---- S^T = K Q^T (16 tokens x 8 heads), 8 k-steps over d
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        {
+            const int r = lane & 15;                       // K row (token) this lane addresses
+            const uint32_t k_lane = kt + (uint32_t)(r * 128);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int ch = kk * 2 + (lane >> 4);       // 16-B chunk of the 256-B row
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(k_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
+                mma_16816_full<DT>(sacc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+            }
+        }
+        // ---- online softmax per head column; rows t8 (c0, c1) and t8 + 8 (c2, c3)
+        const bool v0 = t8 < valid, v1 = t8 + 8 < valid;
+        float x[4];
+        x[0] = v0 ? sacc[0] * scale_log2 : -INFINITY;     // (t8,   head 2tid)
+        x[1] = v0 ? sacc[1] * scale_log2 : -INFINITY;     // (t8,   head 2tid+1)
+        x[2] = v1 ? sacc[2] * scale_log2 : -INFINITY;     // (t8+8, head 2tid)
+        x[3] = v1 ? sacc[3] * scale_log2 : -INFINITY;     // (t8+8, head 2tid+1)
+        float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
+#pragma unroll
+        for (int o_ = 4; o_ < 32; o_ <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o_));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o_));
+        }
+        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
+        const float al0 = ex2_diff(m[0], mn0), al1 = ex2_diff(m[1], mn1);
+        m[0] = mn0;
+        m[1] = mn1;
+        const uint32_t p01 = pack2<DT>(ex2_diff(x[0], mn0), ex2_diff(x[1], mn1));   // P^T rows t8
+        const uint32_t p23 = pack2<DT>(ex2_diff(x[2], mn0), ex2_diff(x[3], mn1));   // P^T rows t8 + 8
+        // l accumulates the same (rounded) p that feeds the P.V product
+        const float2 f01 = unpack2<DT>(p01), f23 = unpack2<DT>(p23);
+        l[0] = l[0] * al0 + (f01.x + f23.x);
+        l[1] = l[1] * al1 + (f01.y + f23.y);
+#pragma unroll
+        for (int md = 0; md < 8; ++md) {
+            o[md][0] *= al0;
+            o[md][1] *= al1;
+            o[md][2] *= al0;
+            o[md][3] *= al1;
+        }
+        const uint32_t b0 = movmatrix_trans(p01), b1 = movmatrix_trans(p23);   // P^T as B (k = tokens)
+        // ---- O^T += V^T P^T: V^T fragments by ldmatrix.trans; invalid tokens' V zeroed (NaN-safe)
+        uint32_t mlo = 0xffffffffu, mhi = 0xffffffffu;
+        if (valid < kTileRows) {
+            mlo = (tid * 2 < valid ? 0x0000ffffu : 0u) | (tid * 2 + 1 < valid ? 0xffff0000u : 0u);
+            mhi = (8 + tid * 2 < valid ? 0x0000ffffu : 0u) | (8 + tid * 2 + 1 < valid ? 0xffff0000u : 0u);
+        }
+        {
+            const int r = (lane & 7) + (lane >> 4) * 8;    // V row (token) this lane addresses
+            const uint32_t v_lane = vt + (uint32_t)(r * 128);
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                const int ch = md * 2 + ((lane >> 3) & 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(v_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
+                mma_16816_full<DT>(o[md], a0 & mlo, a1 & mlo, a2 & mhi, a3 & mhi, b0, b1);
+            }
+        }
+        release();
+    }
+
+    __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
+        const int tid = lane & 3, t8 = lane >> 2;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int o_ = 4; o_ < 32; o_ <<= 1) l[j] += __shfl_xor_sync(0xffffffffu, l[j], o_);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int h = tid * 2 + j;
+            if (h < G) {
+                float *dst = cb_o + ((size_t)wc * G + h) * kHeadDim;
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    dst[md * 16 + t8] = o[md][j];
+                    dst[md * 16 + t8 + 8] = o[md][2 + j];
+                }
+                if (t8 == 0) {
+                    cb_m[wc * G + h] = m[j];
+                    cb_l[wc * G + h] = l[j];
+                }
+            }
+        }
+    }
+};
+
+#ifndef APEX_MMA_T
+#define APEX_MMA_T 1
+#endif
+template <int DT, int G> struct ConsumerSel {
+    using T = typename std::conditional<APEX_MMA_T != 0, MmaConsumerT<DT, G>, MmaConsumer<DT, G>>::type;
+};
 template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
 
 // log-sum-exp merge of one split (b, g) pair, partials combined in split order:

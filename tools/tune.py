@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--chunks", default="0,256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--layers", type=int, default=1, help="physical layers; calls rotate over them")
     ap.add_argument("--scheds", default="", help="comma list of apex_kv_set_sched values (-1 dynamic, "
                                                  "0..1000 stream-K dynamic permille); empty = library default")
     a = ap.parse_args()
@@ -36,9 +37,10 @@ def main():
     B = len(ctx)
     mult = int(os.environ.get("APEX_TUNE_BLOCK_MULT", "1"))     # >1: spare pool rows for layout experiments
     cache = make_cache(w.dtype, w.num_q_heads, w.num_kv_heads, mult * (sum(-(-(c + 1) // 16) for c in ctx) + 16),
-                       max_seqs=B, max_blocks_per_seq=-(-(max(ctx) + 1) // 16) + 1, max_new_tokens=1 << 22)
+                       max_seqs=B, max_blocks_per_seq=-(-(max(ctx) + 1) // 16) + 1, max_new_tokens=1 << 22,
+                       layers=a.layers)
     seqs = list(range(B))
-    prefill(cache, seqs, ctx)
+    prefill(cache, seqs, ctx)            # layer 0 holds data; the other layers' bytes are streamed as they are
     es = 4 if w.dtype == "f32" else 2
     nbytes = sum(c * w.num_kv_heads * 128 * 2 * es for c in ctx) + 2 * B * w.num_q_heads * 128 * es
     res = []
@@ -61,13 +63,13 @@ def main():
                 continue
             q = gen_dev(cache, 0, 0, seqs, [c - 1 for c in ctx], w.num_q_heads)
             out = torch.empty_like(q)
-            for _ in range(3):
-                cache.decode(0, q, out=out)
+            for li in range(max(3, a.layers)):
+                cache.decode(li % a.layers, q, out=out)
             ts = []
-            for _ in range(a.reps):
+            for r in range(a.reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                cache.decode(0, q, out=out)
+                cache.decode(r % a.layers, q, out=out)
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e3)
