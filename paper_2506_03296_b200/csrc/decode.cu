@@ -20,12 +20,13 @@
 //    with one shared ring a fast warp could wait on a slot whose previous fill
 //    was still in flight, and mbarrier try_wait.parity would report the
 //    preceding phase as complete (a race seen at C2 sizes);
-//  * GQA (g >= 2, 16-bit): S = Q_g K^T and O += P V on tensor cores with
-//    mma.sync.m16n8k16 (q-group rows padded to 16; P re-used from the S
-//    accumulator registers as the A operand), K/V fragments via ldmatrix on the
-//    swizzled tiles (conflict-free);
+//  * GQA (g >= 2, 16-bit): S^T = K Q_g^T and O^T += V^T P^T on tensor cores with
+//    mma.sync.m16n8k16, the q-group on the N = 8 side (16 HMMA per 16-token
+//    tile), K/V fragments via ldmatrix(.trans) on the swizzled tiles
+//    (conflict-free), P^T re-laid from the S^T accumulators by movmatrix.trans;
 //  * MHA (g == 1) and fp32: CUDA-core FMAs, one lane per token for q.K
-//    (conflict-free thanks to the swizzle), lane-owned dims for P.V.
+//    (conflict-free thanks to the swizzle), lane-owned dims for P.V (16-bit MHA
+//    uses the tensor-core path in the latency regime).
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
 //    (m, l, unnormalised O) fp32 partials merged in split order -- by a second
 //    small launch (fixed grid, grid-stride over split pairs) in the bandwidth
@@ -61,9 +62,6 @@ namespace {
 #endif
 #ifndef APEX_CTAS_PER_SM
 #define APEX_CTAS_PER_SM 2
-#endif
-#ifndef APEX_EARLY_RELEASE
-#define APEX_EARLY_RELEASE 0
 #endif
 #ifndef APEX_MERGE_UNROLL
 #define APEX_MERGE_UNROLL 16
@@ -184,22 +182,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t 
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
-// D = A(16x16, rows 8..15 zero) * B(16x8) + D, fp32 accumulate
-template <int DT>
-__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
-    const uint32_t z = 0;
-    if constexpr (DT == APEX_BF16)
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(z), "r"(a2), "r"(z), "r"(b0), "r"(b1));
-    else
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(z), "r"(a2), "r"(z), "r"(b0), "r"(b1));
-}
-
 // 16-bit pair <-> floats
 template <int DT> __device__ __forceinline__ float2 unpack2(uint32_t u) {
     if constexpr (DT == APEX_BF16) {
@@ -275,125 +257,6 @@ template <int ES> struct NewRow {
 };
 
 // ------------------------------------------------------------------ consumers
-// Running online-softmax state of one consumer warp for its share of an item.
-// MMA layout: row = lane/4 (q head of the group), 2 columns per n-tile.
-template <int DT, int G> struct MmaConsumer {
-    uint32_t qa[8][2];          // A fragments of Q (rows >= G zero), per k-step: a0, a2
-    float o[16][4];             // O accumulators, n-tile nd covers dims nd*8..nd*8+7
-    float m, l;                 // running max (log2 units) and this thread's partial sum
-
-    // qg: the G q rows of the item's kv head (global memory, or the item's smem q slot)
-    __device__ __forceinline__ void begin(const uint8_t *qg, const DecodeParams &, int lane) {
-        const int row = lane >> 2, tid = lane & 3;
-        const uint32_t *qrow = reinterpret_cast<const uint32_t *>(qg + (size_t)row * kHeadDim * 2);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            qa[kk][0] = row < G ? qrow[kk * 8 + tid] : 0u;
-            qa[kk][1] = row < G ? qrow[kk * 8 + 4 + tid] : 0u;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-        m = -INFINITY;
-        l = 0.f;
-    }
-
-    template <typename Release>
-    __device__ __forceinline__ void tile(uint32_t kt, uint32_t vt, int valid, float scale_log2, int lane,
-                                         Release release) {
-        const int r8 = lane & 7, mi = lane >> 3, tid = lane & 3, row = lane >> 2;
-        // ---- S = Q K^T  (16 x 16 tokens), k-steps over d
-        float s[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        const uint32_t k_lane = kt + (uint32_t)(((mi >> 1) * 8 + r8) * 128);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const int c = (kk & 3) * 2 + (mi & 1);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(k_lane + (kk >> 2) * kSegStride + ((c ^ r8) << 4), b0, b1, b2, b3);
-            mma_16816<DT>(s[0], qa[kk][0], qa[kk][1], b0, b1);
-            mma_16816<DT>(s[1], qa[kk][0], qa[kk][1], b2, b3);
-        }
-#if APEX_EARLY_RELEASE
-        // V fragments to registers now, then hand the slot back before softmax + P.V
-        uint32_t vf[8][4];
-        {
-            const uint32_t v_lane0 = vt + (uint32_t)(((mi & 1) * 8 + r8) * 128);
-#pragma unroll
-            for (int nd = 0; nd < 16; nd += 2) {
-                const int c = (nd & 7) + (mi >> 1);
-                ldsm_x4_t(v_lane0 + (nd >> 3) * kSegStride + ((c ^ r8) << 4), vf[nd / 2][0], vf[nd / 2][1],
-                          vf[nd / 2][2], vf[nd / 2][3]);
-            }
-        }
-        release();
-#endif
-        // ---- online softmax over this tile's 16 tokens (row = lane/4)
-        float x[4];
-        x[0] = (tid * 2 < valid) ? s[0][0] * scale_log2 : -INFINITY;
-        x[1] = (tid * 2 + 1 < valid) ? s[0][1] * scale_log2 : -INFINITY;
-        x[2] = (8 + tid * 2 < valid) ? s[1][0] * scale_log2 : -INFINITY;
-        x[3] = (8 + tid * 2 + 1 < valid) ? s[1][1] * scale_log2 : -INFINITY;
-        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m, mx);
-        const float alpha = ex2_diff(m, m_new);
-        m = m_new;
-        uint32_t a0 = pack2<DT>(ex2_diff(x[0], m_new), ex2_diff(x[1], m_new));
-        uint32_t a2 = pack2<DT>(ex2_diff(x[2], m_new), ex2_diff(x[3], m_new));
-        if (row >= G) a0 = a2 = 0u;   // padded q rows contribute nothing
-        // l accumulates the same (rounded) p that feeds the P.V product
-        const float2 p01 = unpack2<DT>(a0), p23 = unpack2<DT>(a2);
-        l = l * alpha + ((p01.x + p01.y) + (p23.x + p23.y));
-#pragma unroll
-        for (int nd = 0; nd < 16; ++nd) {
-            o[nd][0] *= alpha;
-            o[nd][1] *= alpha;
-        }
-        // ---- O += P V: V fragments via ldmatrix.trans; masked rows zeroed (NaN-safe)
-        uint32_t mlo = 0xffffffffu, mhi = 0xffffffffu;
-        if (valid < kTileRows) {
-            mlo = (tid * 2 < valid ? 0x0000ffffu : 0u) | (tid * 2 + 1 < valid ? 0xffff0000u : 0u);
-            mhi = (8 + tid * 2 < valid ? 0x0000ffffu : 0u) | (8 + tid * 2 + 1 < valid ? 0xffff0000u : 0u);
-        }
-#if APEX_EARLY_RELEASE
-#pragma unroll
-        for (int nd = 0; nd < 16; nd += 2) {
-            mma_16816<DT>(o[nd], a0, a2, vf[nd / 2][0] & mlo, vf[nd / 2][1] & mhi);
-            mma_16816<DT>(o[nd + 1], a0, a2, vf[nd / 2][2] & mlo, vf[nd / 2][3] & mhi);
-        }
-#else
-        const uint32_t v_lane = vt + (uint32_t)(((mi & 1) * 8 + r8) * 128);
-#pragma unroll
-        for (int nd = 0; nd < 16; nd += 2) {
-            const int c = (nd & 7) + (mi >> 1);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(v_lane + (nd >> 3) * kSegStride + ((c ^ r8) << 4), b0, b1, b2, b3);
-            mma_16816<DT>(o[nd], a0, a2, b0 & mlo, b1 & mhi);
-            mma_16816<DT>(o[nd + 1], a0, a2, b2 & mlo, b3 & mhi);
-        }
-        release();
-#endif
-    }
-
-    __device__ __forceinline__ void finish(float *cb_o, float *cb_m, float *cb_l, int wc, int lane) {
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-        const int row = lane >> 2, tid = lane & 3;
-        if (row < G) {
-            float *dst = cb_o + ((size_t)wc * G + row) * kHeadDim;
-#pragma unroll
-            for (int nd = 0; nd < 16; ++nd)
-                *reinterpret_cast<float2 *>(dst + nd * 8 + tid * 2) = make_float2(o[nd][0], o[nd][1]);
-            if (tid == 0) {
-                cb_m[wc * G + row] = m;
-                cb_l[wc * G + row] = l;
-            }
-        }
-    }
-};
-
 // CUDA-core consumer for g == 1 (fp32 or 16-bit).  q.K: lane t (0..15) owns token
 // t, half hh = lane/16 owns dims hh*64..hh*64+63.  P.V: lane owns 8 (16-bit) or
 // 4 (fp32) dims; 16-bit lanes split even/odd tokens by half-warp.
@@ -553,7 +416,7 @@ __device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
     return d;
 }
 template <int DT>
-__device__ __forceinline__ void mma_16816_full(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
     if constexpr (DT == APEX_BF16)
         asm volatile(
@@ -600,7 +463,7 @@ template <int DT, int G> struct MmaConsumerT {
                 const int ch = kk * 2 + (lane >> 4);       // 16-B chunk of the 256-B row
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4(k_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
-                mma_16816_full<DT>(sacc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+                mma_16816<DT>(sacc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
             }
         }
         // ---- online softmax per head column; rows t8 (c0, c1) and t8 + 8 (c2, c3)
@@ -648,7 +511,7 @@ template <int DT, int G> struct MmaConsumerT {
                 const int ch = md * 2 + ((lane >> 3) & 1);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4_t(v_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
-                mma_16816_full<DT>(o[md], a0 & mlo, a1 & mlo, a2 & mhi, a3 & mhi, b0, b1);
+                mma_16816<DT>(o[md], a0 & mlo, a1 & mlo, a2 & mhi, a3 & mhi, b0, b1);
             }
         }
         release();
@@ -679,13 +542,15 @@ template <int DT, int G> struct MmaConsumerT {
     }
 };
 
-#ifndef APEX_MMA_T
-#define APEX_MMA_T 1
-#endif
-template <int DT, int G> struct ConsumerSel {
-    using T = typename std::conditional<APEX_MMA_T != 0, MmaConsumerT<DT, G>, MmaConsumer<DT, G>>::type;
+template <int DT, int G, bool FUSE> struct ConsumerSel { using T = MmaConsumerT<DT, G>; };
+// MHA (g = 1): fp32 on CUDA cores.  16-bit: CUDA cores in the bandwidth regime,
+// the transposed tensor-core path (one live head column: 16 HMMA per tile instead
+// of ~260 FMA/unpack instructions per lane) in the latency regime, where the
+// per-tile latency matters (fp16 batch 8 x 1K: 43 -> 40 us; bandwidth regime C2:
+// 615 -> 622 us, so not there).
+template <int DT, bool FUSE> struct ConsumerSel<DT, 1, FUSE> {
+    using T = typename std::conditional<DT != APEX_F32 && FUSE, MmaConsumerT<DT, 1>, SimtConsumer<DT>>::type;
 };
-template <int DT> struct ConsumerSel<DT, 1> { using T = SimtConsumer<DT>; };
 
 // log-sum-exp merge of one split (b, g) pair, partials combined in split order:
 // M = max m_i, out = sum 2^(m_i-M) O_i / sum 2^(m_i-M) l_i.  Partials written by
@@ -886,7 +751,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     } else {
         // ================= consumers =================
         const int wc = warp - 1;
-        typename ConsumerSel<DT, G>::T st;
+        typename ConsumerSel<DT, G, FUSE>::T st;
         int32_t mc = 0;                       // tiles consumed from this warp's sub-ring
         for (int k = 0;; ++k) {
             const int slot = k % IR, use = k / IR;
