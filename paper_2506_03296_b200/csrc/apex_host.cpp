@@ -198,6 +198,7 @@ struct apex_kv {
     int32_t forced_chunk_blocks = 0;
     int32_t grid_override = 0;
     int32_t dyn_permille = kDefaultDynPermille;   // apex_kv_set_sched
+    int64_t latency_tiles_per_cta = 512;          // latency regime while T <= this * P (APEX_LAT_TILES: tuning)
     int32_t guided[4] = {8, 900, 950, 980};       // guided: T/(g0 P) chunk, halved from permille g1, g2, g3
     int32_t plan_grid = 0;                        // CTAs the last plan was made for (= launch grid)
     std::vector<int32_t> cta_begin;               // [plan_grid + 1]
@@ -252,6 +253,7 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
     kv->sm_count = query_sm_count(kv->host_only);
     kv->ws = layout_for(desc, kv->sm_count);
     kv->seqs.resize(desc->max_seqs);
+    if (const char *e = std::getenv("APEX_LAT_TILES")) kv->latency_tiles_per_cta = std::max(1, std::atoi(e));
     kv->free_stack.resize(desc->num_blocks);
     for (int32_t i = 0; i < desc->num_blocks; ++i) kv->free_stack[i] = desc->num_blocks - 1 - i;
     if (!kv->host_only) {
@@ -473,8 +475,38 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
     bool latency = false, streamk = false;
     if (kv->forced_chunk_blocks > 0) {
         chunk = kv->forced_chunk_blocks;
-    } else if (T <= 64 * P) {
-        chunk = std::max<int64_t>(1, cdiv(T, P));
+    } else if (T <= kv->latency_tiles_per_cta * P) {
+        // chunk minimising the estimated makespan rounds * (largest piece * t_tile +
+        // t_item) over candidate chunks, rounds = ceil(items / P).  ceil(T/P) alone
+        // can cut pairs into just more pieces than CTAs (e.g. 128 pairs of 129
+        // blocks: chunk 56 -> 384 items, a second round for 88 CTAs: 47 us; chunk
+        // 65 -> 256 items: 38 us) or leave 1024 whole pairs at 3.5 rounds.
+        // t_tile ~ 0.34 us (8 KiB at a CTA's share of HBM), t_item ~ 3 us (per-item
+        // cost incl. the split's merge share; fitted on batch 128 x 512: whole pairs
+        // 63.5 us vs halves 70.7 us), in units of 0.01 us.
+        int32_t maxn = 1;
+        for (int32_t b = 0; b < B; ++b) maxn = std::max(maxn, nblks[b]);
+        auto cost = [&](int64_t c) {
+            int64_t n = 0, big = 0;
+            for (int32_t b = 0; b < B; ++b) {
+                const int64_t k = cdiv(nblks[b], c);
+                n += k * Hkv;
+                big = std::max(big, cdiv(nblks[b], k));
+            }
+            return cdiv(n, P) * (big * 34 + 300);
+        };
+        std::vector<int64_t> cand;
+        for (int64_t k = 1; k <= 64; ++k) cand.push_back(cdiv(maxn, k));
+        for (int64_t r = 1; r <= 16; ++r) cand.push_back(std::max<int64_t>(1, cdiv(T, P * r)));
+        int64_t best = -1;
+        chunk = maxn;
+        for (int64_t c : cand) {
+            const int64_t v = cost(c);
+            if (best < 0 || v < best || (v == best && c > chunk)) {
+                best = v;
+                chunk = c;
+            }
+        }
         latency = true;
     } else if (kv->dyn_permille >= 0) {
         streamk = true;

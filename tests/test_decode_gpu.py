@@ -183,8 +183,8 @@ def test_errors_and_unsupported(cuda_lib):
     assert e.value.code in ("ENOBLOCKS", "EINVAL")
 
 
-@pytest.mark.parametrize("dtype,hq,hkv,batch,ctx", [("f16", 32, 32, 16, 4096), ("bf16", 32, 8, 32, 8192),
-                                                   ("f32", 32, 32, 8, 4096)])
+@pytest.mark.parametrize("dtype,hq,hkv,batch,ctx", [("f16", 32, 32, 20, 4096), ("bf16", 32, 8, 40, 8192),
+                                                   ("f32", 32, 32, 20, 4096)])   # T > 512 P: bandwidth regime
 def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
     """Regression: with one shared tile ring, a fast consumer warp could pass a
     try_wait.parity on a slot whose previous fill was still in flight (seen as a
@@ -195,6 +195,7 @@ def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
     seqs = list(range(batch))
     prefill(cache, seqs, [ctx] * batch)
     out = decode_step(cache, seqs, [ctx] * batch)
+    assert cache.decode_launches() == 2
     q = gen_dev(cache, 0, 0, seqs, [ctx - 1] * batch, hq)
     for _ in range(20):
         again = cache.decode(0, q)
@@ -211,12 +212,12 @@ def test_bandwidth_regime_ring_regression(cuda_lib, dtype, hq, hkv, batch, ctx):
 def test_streamk_schedules(cuda_lib, dtype, hq, hkv, sched, grid):
     """Stream-K static ranges (+ queue tail) in the bandwidth regime: ragged pairs
     cut at CTA range boundaries are merged like split pairs; parity vs the oracle."""
-    ctx = [1000, 3000, 17, 5000, 1, 2500, 4097] if grid == 7 else [20000, 1, 33, 9000, 16000, 12000, 7000, 30001]
+    ctx = [1000, 3000, 17, 5000, 1, 2500, 4097] if grid == 7 else [80000, 1, 33, 36000, 64000, 48000, 28000, 120001]
     cache, seqs, out = run_case(dtype, hq, hkv, ctx, sched=sched, grid=grid or None, interleave=37, seed=3)
     P = len(cache.plan_ranges()) - 1
     assert P == (7 if grid == 7 else 2 * torch_sm_count())
     T = sum(-(-c // 16) for c in ctx) * hkv
-    assert cache.decode_launches() == (2 if T > 64 * P else 1)   # bandwidth regime (+ merge kernel)
+    assert cache.decode_launches() == (2 if T > 512 * P else 1)   # bandwidth regime (+ merge kernel)
     rows = None if grid == 7 else list(range(0, len(ctx) * hq, 3))
     ref = oracle_rows(seqs, ctx, hq, hkv, dtype, seed=3, rows=rows)
     got = out.reshape(-1, 128)[rows] if rows is not None else out

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("dtype,hq,hkv,ctx", [("bf16", 32, 8, [5, 700, 2000, 31]), ("f16", 8, 8, [100, 3000]),
                                               ("f32", 4, 4, [15, 64, 999]),
-                                              ("bf16", 32, 8, [8192] * 16)])   # bandwidth regime + merges
+                                              ("bf16", 32, 8, [8192] * 40)])   # bandwidth regime + merges
 @pytest.mark.parametrize("fused_append", [False, True])
 def test_graph_replay_matches_eager_and_oracle(cuda_lib, dtype, hq, hkv, ctx, fused_append):
     import torch

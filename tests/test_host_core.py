@@ -180,8 +180,8 @@ def test_planner_streamk_ranges():
         items, nm = _check_plan(c, lens, hkv)
         cb = c.plan_ranges()
         assert len(cb) == P + 1
-        if T <= 64 * P:
-            continue                                   # latency regime: one item per CTA, no stream-K
+        if c.decode_launches() == 1:
+            continue                                   # latency regime (fused merge): no stream-K
         t_st = T - T * perm // 1000
         flat = [(b, g, j) for b, L in enumerate(lens) for g in range(hkv) for j in range(-(-L // 16))]
         pos = 0
@@ -209,15 +209,22 @@ def test_planner_split_chunk_and_auto():
     c2.set_grid(296)
     c2.alloc(list(range(4)), [16000] * 4)            # 32 pairs of 1000 blocks: must split (32 << 296 CTAs)
     items, nm = _check_plan(c2, [16000] * 4, 8)
-    assert len(items) >= 296 and nm == 32
+    # latency regime (T = 32000 <= 512 P): one round, 9 pieces per pair (288 <= 296 CTAs)
+    assert len(items) == 288 and nm == 32 and max(it[3] for it in items) == 112
+    assert c2.decode_launches() == 1
+    cb = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=21000, max_blocks_per_seq=1300, max_new_tokens=1 << 20)
+    cb.set_grid(296)
+    cb.alloc(list(range(16)), [20000] * 16)          # T = 160000 > 512 P: bandwidth regime (guided split)
+    items, nm = _check_plan(cb, [20000] * 16, 8)
+    assert len(items) >= 296 and nm == 128 and cb.decode_launches() == 2
     c3 = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=20000, max_blocks_per_seq=1024)
     c3.set_grid(296)
     assert A.apex_kv_decode_launches(c3.handle) == -1
-    c3.alloc([0], [1000])                            # T = 63*8 = 504 <= 64P: ~1 item per CTA
+    c3.alloc([0], [1000])                            # T = 63*8 = 504 <= 512 P: ~1 item per CTA
     items, nm = _check_plan(c3, [1000], 8)
     assert len(items) == 8 * 32 and all(it[3] == 2 for it in items[:-8])
     assert c3.decode_launches() == 1                 # latency regime: merge fused in-kernel
-    assert c2.decode_launches() == 2                 # bandwidth regime with splits: + merge kernel
+    assert cb.decode_launches() == 2                 # bandwidth regime with splits: + merge kernel
     with pytest.raises(A.ApexError):
         c2.set_split(10)                             # not a multiple of 16
 
