@@ -394,12 +394,14 @@ apex_status apex_kv_plan(const apex_kv *kv, int32_t *items, int32_t cap, int32_t
 // tiles, P = persistent CTAs.  Each (row, kv-head) pair is cut into
 // near-equal pieces of at most `chunk` blocks; items run longest-first from
 // the device queue (greedy LPT on P CTAs).
-//  * latency regime (T <= 64 P): chunk = ceil(T/P), about one item per CTA, and
-//    the LSE merge is fused into the decode kernel (saves a launch);
-//  * bandwidth regime: chunk = max(16, ceil(T/16P)) -- ~16 items per CTA keeps
-//    the LPT tail short while per-item costs stay ~1% (tools/tune.py sweeps);
-//    the 16-tile floor matters for few long pairs (e.g. batch 1 at 64K tokens);
-//    pairs shorter than the chunk stay whole (e.g. C5: no split at all);
+//  * latency regime (T <= 512 P): chunk from a makespan model (few rounds of
+//    near-equal items, whole pairs when cheaper), and the LSE merge is fused
+//    into the decode kernel (one launch; the merging CTA's stall is at the end);
+//  * bandwidth regime, guided (default): chunk = max(16, ceil(T/8P)), halved /
+//    quartered / eighthed for the pairs holding the last 10 / 5 / 2% of the
+//    tiles, so the longest-first queue ends with small items; uniform
+//    (apex_kv_set_sched(-1)): chunk = max(16, ceil(T/16P)); stream-K ranges
+//    (apex_kv_set_sched(>= 0)); pairs shorter than the chunk stay whole;
 //  * a forced chunk (apex_kv_set_split) is used as is.
 // A pair cut into >1 pieces gets partial slots and a merge entry.
 namespace {
