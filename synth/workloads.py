@@ -24,7 +24,7 @@ class Workload:
     head_dim: int
     dtype: str
     layers: int
-    ctx_kind: str                 # "uniform" | "hash"
+    ctx_kind: str                 # "uniform" | "hash" | "skew"
     ctx: int = 0                  # uniform context
     ctx_lo: int = 1024            # hash draw: lo + splitmix64(b) % span
     ctx_span: int = 31745
@@ -42,6 +42,8 @@ class Workload:
         b = np.arange(b0, b0 + n, dtype=np.uint64)
         if self.ctx_kind == "uniform":
             return np.full(n, self.ctx, dtype=np.int64)
+        if self.ctx_kind == "skew":                     # request 0 long, the rest short
+            return np.where(b == 0, self.ctx, self.ctx_lo).astype(np.int64)
         return (self.ctx_lo + (splitmix64(b) % np.uint64(self.ctx_span))).astype(np.int64)
 
 
@@ -54,6 +56,9 @@ WORKLOADS = {
                    128, 32, 8, 128, "bf16", 32, "uniform", ctx=8192),
     "c4": Workload("c4", "long-output CoT mix: batch 256, ragged contexts 1K-32K, LLaMA-3.1-8B GQA, bf16, continuous kv_append per step",
                    256, 32, 8, 128, "bf16", 32, "hash", steps=64),
+    # load-balance stress variant of C4: 1 x 32K + 255 x 1K; not a BASELINE config
+    "c4s": Workload("c4s", "C4 skew variant: batch 256, one 32K context + 255 x 1K, LLaMA-3.1-8B GQA, bf16",
+                    256, 32, 8, 128, "bf16", 32, "skew", ctx=32768, ctx_lo=1024),
     "c5": Workload("c5", "LLaMA-3.1-8B GQA, batch 1024, context 16K, all 32 layers, sharded across 1/2/4/8 B200",
                    1024, 32, 8, 128, "bf16", 32, "uniform", ctx=16384),
 }

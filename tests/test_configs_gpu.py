@@ -3,7 +3,8 @@ launch configuration bench.py times (automatic split planner, persistent grid).
 
 C1 is checked on every row (fp32, q x1 and q x8); C2-C5 on >= 256 sampled rows
 (8 whole requests x all q heads, including the shortest and longest contexts of
-the ragged C4) against the float64 oracle on regenerated inputs (readings c6-c8).
+the ragged C4 and the long request of the C4 skew variant c4s) against the
+float64 oracle on regenerated inputs (readings c6-c8).
 """
 import numpy as np
 import pytest
@@ -40,7 +41,7 @@ def test_c1_full(cuda_lib, qamp):
     check_close(out, ref, "f32")
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c5", "c4s"])
 def test_uniform_configs_sampled(cuda_lib, name):
     import torch
     w, cache, seqs, ctx = build(name)
