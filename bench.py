@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--append", choices=["fused", "separate"], default="fused",
                     help="fused: apex_decode_attention_append (append inside the decode launch); "
                          "separate: apex_kv_append + apex_decode_attention")
+    ap.add_argument("--sched", type=int, default=None,
+                    help="planner schedule override (apex_kv_set_sched): -2 guided (library default), "
+                         "-1 uniform dynamic split, 0..1000 stream-K")
     ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
                     help="head mode: NCCL all_gather_into_tensor, or stores into peers' symmetric memory "
                          "from the decode epilogue (experimental, needs >= 2 GPUs)")
@@ -313,6 +316,8 @@ def run_apex(args):
     cache = PagedKVCache(num_layers=P, num_q_heads=hq, num_kv_heads=hkv, num_blocks=blocks_per_layer,
                          max_seqs=B, max_blocks_per_seq=mbps, max_batch=B,
                          max_new_tokens=max(chunk_rows, B) + int(ctx0.max()), dtype=dt, device=dev)
+    if args.sched is not None:
+        cache.set_sched(args.sched)
     seq = list(range(B))                              # handle-local sequence ids = batch rows
     gid = torch.as_tensor(ids.astype(np.int32), device=dev)
 
@@ -471,7 +476,8 @@ def run_apex(args):
                                 f"{l2_bytes / 2**20:.0f} MiB L2, so a 512 MiB buffer is written before every "
                                 "step (outside the per-step events; time = sum of per-step intervals)"),
                          "work_items_per_layer": n_items, "split_merges_per_layer": n_merges,
-                         "append": "fused into the decode launch (apex_decode_attention_append)" if fused_append
+                         "append": ("apex_decode_attention_append (latency regime: inside the decode launch; "
+                                    "bandwidth regime: append kernel + decode kernel)") if fused_append
                                    else "separate apex_kv_append launch"},
               "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,
               "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
@@ -481,7 +487,9 @@ def run_apex(args):
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
-              "gpu_launches": K * (1 + L * ((0 if fused_append else 1) + decode_launches)),   # deltas + L x ([append,] decode[, merge])
+              # deltas + L x ([append,] decode[, merge]); the append rides in the decode launch only
+              # in the latency regime (decode_launches == 1)
+              "gpu_launches": K * (1 + L * ((0 if fused_append and decode_launches == 1 else 1) + decode_launches)),
               "prefill_s": t_fill}
     if clk:
         result["clocks"] = clk

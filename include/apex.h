@@ -159,12 +159,14 @@ apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, 
 /* apex_kv_append + apex_decode_attention in ONE launch for
    a pure decode step: every sequence of the last apex_kv_alloc has exactly one
    new token (else APEX_EINVAL, nothing enqueued).  k_new / v_new: device
-   [batch][Hkv][D] in the step's row order, 16-byte aligned.  The CTA that
-   streams a sequence's last block writes the new K/V row into the pool (so
-   later steps see it, exactly as apex_kv_append would) and patches it into its
-   shared-memory copy of the tile before use; outputs and pools are
-   bit-identical to the two-call sequence.  Other arguments as
-   apex_decode_attention. */
+   [batch][Hkv][D] in the step's row order, 16-byte aligned.  Latency regime
+   (apex_kv_decode_launches() == 1): ONE launch -- the CTA that streams a
+   sequence's last block writes the new K/V row into the pool (so later steps
+   see it, exactly as apex_kv_append would) and patches it into its
+   shared-memory copy of the tile before use.  Bandwidth regime: the append
+   kernel then the plain decode kernel (measured faster there).  Either way
+   outputs and pools are bit-identical to the two-call sequence.  Other
+   arguments as apex_decode_attention. */
 apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void *q, const void *k_new,
                                          const void *v_new, void *out, float scale, apex_stream stream);
 

@@ -782,10 +782,22 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
         if (!kv->single_token_step)
             return fail(APEX_EINVAL, "fused append needs exactly one new token per sequence in the step "
                                      "(use apex_kv_append + apex_decode_attention)");
-        p.k_new = k_new;
-        p.v_new = v_new;
-        p.kv_pool = kv->kv_pools[layer];
-        p.num_blocks = kv->d.num_blocks;
+        if (kv->fuse_merge) {
+            // latency regime: the append rides in the decode launch (one launch per call)
+            p.k_new = k_new;
+            p.v_new = v_new;
+            p.kv_pool = kv->kv_pools[layer];
+            p.num_blocks = kv->d.num_blocks;
+        } else {
+            // bandwidth regime: the separate append kernel + the plain decode kernel is
+            // faster than the fused-append decode kernel (whose per-tile checks and row
+            // patch cost 2-6% of a 4-64 GiB stream, more than the saved launch)
+            uint8_t *up = (uint8_t *)kv->d.workspace + kv->ws.upload;
+            cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->kv_pools[layer],
+                                                (const int32_t *)(up + kv->ws.o_tail), (const apex::StepHeader *)up,
+                                                kv->d.num_kv_heads, kv->sm_count, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "apex_decode_attention_append (append)");
+        }
     }
     // fixed persistent grid (CTAs without an item exit at once): every launch parameter is
     // step-invariant, so the per-layer launches can be captured in a CUDA graph

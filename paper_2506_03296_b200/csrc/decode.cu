@@ -63,6 +63,20 @@ namespace {
 #ifndef APEX_CTAS_PER_SM
 #define APEX_CTAS_PER_SM 2
 #endif
+#ifndef APEX_SPEC_ITEM
+#define APEX_SPEC_ITEM 1
+#endif
+#ifndef APEX_MSCR_ALL
+#define APEX_MSCR_ALL 0
+#endif
+#ifndef APEX_Q_LDG
+#define APEX_Q_LDG 0
+#endif
+#if APEX_Q_LDG
+#define LDQ(p) __ldg(p)
+#else
+#define LDQ(p) (*(p))
+#endif
 #ifndef APEX_MERGE_UNROLL
 #define APEX_MERGE_UNROLL 16
 #endif
@@ -89,14 +103,14 @@ struct ItemSlot {
 
 constexpr int kSmemPerCta = (232448 - 1024 * CTAS_PER_SM) / CTAS_PER_SM - 1024;   // SM carve-out split
 
-template <int DT, int G> struct Cfg {
+template <int DT, int G, bool FUSE = true> struct Cfg {
     static constexpr int ES = DT == APEX_F32 ? 4 : 2;
     static constexpr int TILE = kTileRows * kHeadDim * ES;   // bytes of the K (or the V) half of a tile
     static constexpr int CB_O = NC * G * kHeadDim * 4;       // per-warp O for the item merge
     static constexpr int CB_ML = NC * G * 2 * 4 + 16;     // + merge flag
-    static constexpr int MSCR = NC * 32 * (16 + 8);        // fused merge: red (float4) + redml (float2) per thread
+    static constexpr int MSCR = (FUSE || APEX_MSCR_ALL) ? NC * 32 * (16 + 8) : 0;   // fused merge: red + redml per thread
     static constexpr int RING = IR * (int)sizeof(ItemSlot);
-    static constexpr int FIXED = CB_O + CB_ML + NC * 32 * 24 + RING + 2 * IR * 8 + 1024;
+    static constexpr int FIXED = CB_O + CB_ML + MSCR + RING + 2 * IR * 8 + 1024;
     static constexpr int S0 = (kSmemPerCta - FIXED) / (2 * TILE + 16);
     static constexpr int SW = (S0 > APEX_MAX_SLOTS ? APEX_MAX_SLOTS : S0) / NC;   // slots per consumer warp
     static constexpr int STAGES = SW * NC;
@@ -273,7 +287,7 @@ template <int DT> struct SimtConsumer {
             const float4 *src = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(qg) + base);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                float4 v = src[i];
+                float4 v = LDQ(src + i);
                 qv[4 * i] = v.x * p.scale_log2;
                 qv[4 * i + 1] = v.y * p.scale_log2;
                 qv[4 * i + 2] = v.z * p.scale_log2;
@@ -283,7 +297,7 @@ template <int DT> struct SimtConsumer {
             const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint16_t *>(qg) + base);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                uint4 v = src[i];
+                uint4 v = LDQ(src + i);
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -440,8 +454,8 @@ template <int DT, int G> struct MmaConsumerT {
         const uint32_t *qrow = reinterpret_cast<const uint32_t *>(qg + (size_t)h * kHeadDim * 2);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-            qb[kk][0] = h < G ? qrow[kk * 8 + tid] : 0u;
-            qb[kk][1] = h < G ? qrow[kk * 8 + 4 + tid] : 0u;
+            qb[kk][0] = h < G ? LDQ(qrow + kk * 8 + tid) : 0u;
+            qb[kk][1] = h < G ? LDQ(qrow + kk * 8 + 4 + tid) : 0u;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -620,11 +634,11 @@ __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeIte
 }
 
 // ------------------------------------------------------------------ decode kernel
-template <int DT, int G, bool FUSE>
+template <int DT, int G, bool FUSE, bool AP>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     apex_decode_kernel(const __grid_constant__ CUtensorMap tmkv,
                        const DecodeParams p) {
-    using C = Cfg<DT, G>;
+    using C = Cfg<DT, G, FUSE>;
     using S = C;
     constexpr int STAGES = C::STAGES, TILE = C::TILE;
     extern __shared__ uint8_t smem_raw[];
@@ -697,7 +711,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
-            const WorkItem it = (k == 0 && idx == (int)blockIdx.x) ? spec : p.items[idx];
+            const WorkItem it = (APEX_SPEC_ITEM && k == 0 && idx == (int)blockIdx.x) ? spec : p.items[idx];
             if (lane == 0) {
                 ring[slot].it = it;
                 mbar_arrive(ifull0 + 8 * slot);
@@ -715,7 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 #endif
                 for (int jj = 0; jj < cnt; ++jj) {
                     const int phys = __shfl_sync(0xffffffffu, my, jj);
-                    if (p.k_new && it.blk0 + j0 + jj == (it.len - 1) / kTileRows)   // fused append
+                    if (AP && it.blk0 + j0 + jj == (it.len - 1) / kTileRows)   // fused append
                         NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
                     const int w = (j0 + jj) % NC;
                     int m = 0;
@@ -771,7 +785,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 #endif
                 const int valid = min(kTileRows, it.len - (it.blk0 + j) * kTileRows);
                 const uint32_t kt = tiles_u + s * 2 * TILE;
-                if (p.k_new && it.blk0 + j == (it.len - 1) / kTileRows)   // fused append: patch the new row
+                if (AP && it.blk0 + j == (it.len - 1) / kTileRows)   // fused append: patch the new row
                     NewRow<C::ES>::to_tile(p, it.b, it.g, kt, (it.len - 1) % kTileRows, lane);
                 st.tile(kt, kt + kVOff, valid, p.scale_log2, lane, [&] {
                     __syncwarp();                                 // every lane's smem reads of the slot are done
@@ -853,7 +867,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 
 // log-sum-exp merge of split pairs as its own launch (bandwidth regime): one CTA
 // per (b, g) pair, so merging never stalls a decode CTA's TMA stream.
-constexpr int kMergeThreads = 512;
+// 128 threads: the bandwidth regime's merges have small fan-in (guided split:
+// <= ~20 parts) and many pairs (C3: 1024), so CTA count per wave matters more
+// than part groups (512 threads: 13.4 us per C3 layer vs 9.9 us); large fan-in
+// occurs only in the latency regime, merged in-kernel.
+constexpr int kMergeThreads = 128;
 template <int DT, int G>
 __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeParams p) {
     __shared__ float4 red[kMergeThreads];                   // part-group partials (G * 32 * ngr)
@@ -866,11 +884,18 @@ __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeP
 }
 
 template <int DT, int G> cudaError_t prepare() {
-    cudaError_t e = cudaFuncSetAttribute(apex_decode_kernel<DT, G, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<DT, G>::TOTAL);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(apex_decode_kernel<DT, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                Cfg<DT, G>::TOTAL);
+    // AP (fused append) is a separate instantiation: its per-tile checks and row
+    // copies cost the plain kernel ~8% at C5 sizes when compiled in (measured)
+    const void *k[4] = {(const void *)apex_decode_kernel<DT, G, false, false>,
+                        (const void *)apex_decode_kernel<DT, G, false, true>,
+                        (const void *)apex_decode_kernel<DT, G, true, false>,
+                        (const void *)apex_decode_kernel<DT, G, true, true>};
+    const int sm[4] = {Cfg<DT, G, false>::TOTAL, Cfg<DT, G, false>::TOTAL, Cfg<DT, G>::TOTAL, Cfg<DT, G>::TOTAL};
+    for (int i = 0; i < 4; ++i) {
+        cudaError_t e = cudaFuncSetAttribute(k[i], cudaFuncAttributeMaxDynamicSharedMemorySize, sm[i]);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // Decode and merge kernels are launched with programmatic dependent launch:
@@ -895,11 +920,16 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, 
 template <int DT, int G>
 cudaError_t launch(const TmaMap &tm, const DecodeParams &p, int grid, cudaStream_t s) {
     if (grid > 0) {
-        cudaError_t e = p.fuse_merge
-                            ? launch_pdl(apex_decode_kernel<DT, G, true>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.kv,
-                                         p)
-                            : launch_pdl(apex_decode_kernel<DT, G, false>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s,
-                                         tm.kv, p);
+        const bool ap = p.k_new != nullptr;
+        cudaError_t e;
+        if (p.fuse_merge)
+            e = ap ? launch_pdl(apex_decode_kernel<DT, G, true, true>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.kv, p)
+                   : launch_pdl(apex_decode_kernel<DT, G, true, false>, grid, NTHREADS, Cfg<DT, G>::TOTAL, s, tm.kv, p);
+        else
+            e = ap ? launch_pdl(apex_decode_kernel<DT, G, false, true>, grid, NTHREADS, Cfg<DT, G, false>::TOTAL, s,
+                                tm.kv, p)
+                   : launch_pdl(apex_decode_kernel<DT, G, false, false>, grid, NTHREADS, Cfg<DT, G, false>::TOTAL, s,
+                                tm.kv, p);
         if (e != cudaSuccess || p.fuse_merge) return e;
     }
     // launched whenever merges are not fused, even if this step has none (it then
