@@ -71,14 +71,17 @@ def prefill(cache, seq_ids, ctx, layer=0, seed=0, interleave=0, max_rows=1 << 22
             cache.append(l, k, v)
 
 
-def decode_step(cache, seq_ids, ctx, layer=0, seed=0, qamp=1.0, scale=None):
-    """alloc(+1), append the step's token (pos ctx-1), decode; returns out (torch)."""
+def decode_step(cache, seq_ids, ctx, layer=0, seed=0, qamp=1.0, scale=None, fused_append=False):
+    """alloc(+1), append the step's token (pos ctx-1), decode; returns out (torch).
+    fused_append: one apex_decode_attention_append call instead of append + decode."""
     cache.alloc(list(seq_ids), [1] * len(seq_ids))
     pos = [c - 1 for c in ctx]
     k = gen_dev(cache, TENSOR_K, layer, seq_ids, pos, cache.num_kv_heads, seed)
     v = gen_dev(cache, TENSOR_V, layer, seq_ids, pos, cache.num_kv_heads, seed)
-    cache.append(layer, k, v)
     q = gen_dev(cache, TENSOR_Q, layer, seq_ids, pos, cache.num_q_heads, seed, qamp)
+    if fused_append:
+        return cache.decode_append(layer, q, k, v, scale=scale)
+    cache.append(layer, k, v)
     return cache.decode(layer, q, scale=scale)
 
 
