@@ -356,8 +356,10 @@ template <int DT> struct SimtConsumer {
         m = m_new;
         const float pt = ex2_diff(x, m_new);
         l = l * alpha + pt;
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {   // bit-identical skip when the max did not move
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] *= alpha;
+            for (int i = 0; i < 8; ++i) o[i] *= alpha;
+        }
         // ---- O += p_r V_r over lane-owned dims
         if constexpr (F32) {
             const int sg = lane >> 3, c = lane & 7;
@@ -472,11 +474,11 @@ template <int DT, int G> struct MmaConsumerT {
         {
             const int r = lane & 15;                       // K row (token) this lane addresses
             const uint32_t k_lane = kt + (uint32_t)(r * 128);
+            const int cx = (lane >> 4) ^ (r & 7);          // chunk kk*2 + (lane >> 4), swizzled
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                const int ch = kk * 2 + (lane >> 4);       // 16-B chunk of the 256-B row
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4(k_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
+                ldsm_x4(k_lane + (kk >> 2) * kSegStride + ((((kk & 3) * 2) ^ cx) << 4), a0, a1, a2, a3);
                 mma_16816<DT>(sacc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
             }
         }
@@ -503,12 +505,16 @@ template <int DT, int G> struct MmaConsumerT {
         const float2 f01 = unpack2<DT>(p01), f23 = unpack2<DT>(p23);
         l[0] = l[0] * al0 + (f01.x + f23.x);
         l[1] = l[1] * al1 + (f01.y + f23.y);
+        // rescale only when some head's running max moved (alpha == 1 exactly otherwise,
+        // so skipping is bit-identical; after the first tiles it rarely moves)
+        if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
 #pragma unroll
-        for (int md = 0; md < 8; ++md) {
-            o[md][0] *= al0;
-            o[md][1] *= al1;
-            o[md][2] *= al0;
-            o[md][3] *= al1;
+            for (int md = 0; md < 8; ++md) {
+                o[md][0] *= al0;
+                o[md][1] *= al1;
+                o[md][2] *= al0;
+                o[md][3] *= al1;
+            }
         }
         const uint32_t b0 = movmatrix_trans(p01), b1 = movmatrix_trans(p23);   // P^T as B (k = tokens)
         // ---- O^T += V^T P^T: V^T fragments by ldmatrix.trans; invalid tokens' V zeroed (NaN-safe)
@@ -519,13 +525,23 @@ template <int DT, int G> struct MmaConsumerT {
         }
         {
             const int r = (lane & 7) + (lane >> 4) * 8;    // V row (token) this lane addresses
+            // 16-B column of m-tile md: ((md % 4) * 2 + b) ^ (r & 7) = ((md % 4) * 2) ^ cx
             const uint32_t v_lane = vt + (uint32_t)(r * 128);
+            const int cx = ((lane >> 3) & 1) ^ (r & 7);
+            if (valid == kTileRows) {                     // full tile: no masking (uniform branch)
 #pragma unroll
-            for (int md = 0; md < 8; ++md) {
-                const int ch = md * 2 + ((lane >> 3) & 1);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(v_lane + (ch >> 3) * kSegStride + (((ch & 7) ^ (r & 7)) << 4), a0, a1, a2, a3);
-                mma_16816<DT>(o[md], a0 & mlo, a1 & mlo, a2 & mhi, a3 & mhi, b0, b1);
+                for (int md = 0; md < 8; ++md) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(v_lane + (md >> 2) * kSegStride + ((((md & 3) * 2) ^ cx) << 4), a0, a1, a2, a3);
+                    mma_16816<DT>(o[md], a0, a1, a2, a3, b0, b1);
+                }
+            } else {
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(v_lane + (md >> 2) * kSegStride + ((((md & 3) * 2) ^ cx) << 4), a0, a1, a2, a3);
+                    mma_16816<DT>(o[md], a0 & mlo, a1 & mlo, a2 & mhi, a3 & mhi, b0, b1);
+                }
             }
         }
         release();
