@@ -665,32 +665,35 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         kv->staged_pending[r] = false;
     }
     uint8_t *host = kv->staging[r];
-    const apex::StepHeader hdr{(int32_t)kv->items.size(), (int32_t)kv->merges.size(), (int32_t)rows, 0};
-    std::memcpy(host, &hdr, sizeof hdr);
-    std::memcpy(host + apex::kCtaBeginOffset, kv->cta_begin.data(), sizeof(int32_t) * kv->cta_begin.size());
+    // packed: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
+    // len deltas -- one H2D copy of exactly the used bytes; kernels find the merge
+    // list and the slot map through offsets in the header (fixed launch parameters)
     const size_t items_bytes = sizeof(WorkItem) * kv->items.size();
     const size_t merges_bytes = sizeof(MergeItem) * kv->merges.size();
+    std::memcpy(host + apex::kCtaBeginOffset, kv->cta_begin.data(), sizeof(int32_t) * kv->cta_begin.size());
     std::memcpy(host + kv->ws.o_items, kv->items.data(), items_bytes);
-    if (merges_bytes) std::memcpy(host + kv->ws.o_merges, kv->merges.data(), merges_bytes);
-    size_t off = kv->ws.o_tail;
+    size_t off = align_up(kv->ws.o_items + items_bytes, 256);
     auto put = [&](const void *src, size_t bytes) {
         const size_t at = off;
         if (bytes) std::memcpy(host + at, src, bytes);
         off = align_up(off + bytes, 256);
         return at;
     };
-    put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
+    const size_t o_merges = put(kv->merges.data(), merges_bytes);
+    const size_t o_slots = put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
     const size_t o_bt = put(bt_delta.data(), sizeof(int2) * bt_delta.size());
     const size_t o_len = put(len_delta.data(), sizeof(int2) * len_delta.size());
+    if (off > kv->ws.upload_cap) return fail(APEX_EINVAL, "step metadata exceeds the upload region");
+    apex::StepHeader hdr{};
+    hdr.n_items = (int32_t)kv->items.size();
+    hdr.n_merges = (int32_t)kv->merges.size();
+    hdr.n_rows = (int32_t)rows;
+    hdr.o_merges = (int32_t)o_merges;
+    hdr.o_slots = (int32_t)o_slots;
+    std::memcpy(host, &hdr, sizeof hdr);
     uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
     cudaStream_t s = (cudaStream_t)stream;
-    // header + items | merges | tail: three copies of exactly the used bytes
-    cudaError_t e = cudaMemcpyAsync(dev, host, kv->ws.o_items + items_bytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && merges_bytes)
-        e = cudaMemcpyAsync(dev + kv->ws.o_merges, host + kv->ws.o_merges, merges_bytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(dev + kv->ws.o_tail, host + kv->ws.o_tail, off - kv->ws.o_tail, cudaMemcpyHostToDevice,
-                            s);
+    cudaError_t e = cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
     if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: metadata upload");
     kv->staged_pending[r] = true;
@@ -720,7 +723,7 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
     // always one launch (it reads the row count from the step header): graph-capturable
     uint8_t *up = (uint8_t *)kv->d.workspace + kv->ws.upload;
     cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->kv_pools[layer],
-                                        (const int32_t *)(up + kv->ws.o_tail), (const apex::StepHeader *)up,
+                                        nullptr, (const apex::StepHeader *)up,
                                         kv->d.num_kv_heads, kv->sm_count, (cudaStream_t)stream);
     return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_kv_append");
 }
@@ -764,7 +767,7 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
     p.hdr = (const apex::StepHeader *)up;
     p.cta_begin = (const int32_t *)(up + apex::kCtaBeginOffset);
     p.items = (const WorkItem *)(up + kv->ws.o_items);
-    p.merges = (const MergeItem *)(up + kv->ws.o_merges);
+    p.merges = nullptr;                 // device side: hdr->o_merges (packed upload)
     p.part_o = (float *)(ws + kv->ws.part_o);
     p.part_ml = (float *)(ws + kv->ws.part_ml);
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
@@ -794,7 +797,7 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
             // patch cost 2-6% of a 4-64 GiB stream, more than the saved launch)
             uint8_t *up = (uint8_t *)kv->d.workspace + kv->ws.upload;
             cudaError_t e = apex::launch_append(kv->d.dtype, k_new, v_new, kv->kv_pools[layer],
-                                                (const int32_t *)(up + kv->ws.o_tail), (const apex::StepHeader *)up,
+                                                nullptr, (const apex::StepHeader *)up,
                                                 kv->d.num_kv_heads, kv->sm_count, (cudaStream_t)stream);
             if (e != cudaSuccess) return cuda_fail(e, "apex_decode_attention_append (append)");
         }

@@ -43,13 +43,15 @@ struct __align__(16) StepHeader {
     int32_t n_items;
     int32_t n_merges;
     int32_t n_rows;       // new-token rows of the step (append)
-    int32_t pad;
+    int32_t o_merges;     // byte offsets from the header of this step's merge list and slot map:
+    int32_t o_slots;      // the upload is packed (ONE H2D copy per step); kernels derive the
+    int32_t pad[3];       // pointers on the device, so their launch parameters stay fixed
 };
 // Right after the header (at byte kCtaBeginOffset of the upload region): int32
 // cta_begin[grid + 1].  CTA c first runs items [cta_begin[c], cta_begin[c+1])
 // (its static range), then pulls items cta_begin[grid] + atomicAdd(queue) until
 // the list ends.
-constexpr int kCtaBeginOffset = 16;
+constexpr int kCtaBeginOffset = 32;
 
 struct DecodeParams {
     const void *q;             // [B][Hq][D]
@@ -59,7 +61,7 @@ struct DecodeParams {
     int32_t n_out;
     const int32_t *block_table;
     const WorkItem *items;
-    const MergeItem *merges;
+    const MergeItem *merges;   // unused (the kernels derive the list from hdr->o_merges)
     float *part_o;             // [slots][G][D]   unnormalised sum_t p_t v_t (fp32)
     float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)
     int32_t *counters;         // [2]: work-queue head, CTAs done

@@ -12,10 +12,12 @@ namespace {
 
 __global__ void __launch_bounds__(256) apex_append_kernel(const uint4 *__restrict__ k_new,
                                                           const uint4 *__restrict__ v_new, uint4 *__restrict__ kv_pool,
-                                                          const int32_t *__restrict__ slots,
+                                                          const int32_t *slots,
                                                           const StepHeader *__restrict__ hdr, int hkv,
                                                           int chunks_per_vec) {
     const int n_rows = hdr->n_rows;                       // step count from the device header
+    if (!slots)                                           // packed upload: slot map after the merge list
+        slots = reinterpret_cast<const int32_t *>(reinterpret_cast<const uint8_t *>(hdr) + hdr->o_slots);
     const int64_t per_tensor = (int64_t)n_rows * hkv * chunks_per_vec;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * per_tensor; i += stride) {

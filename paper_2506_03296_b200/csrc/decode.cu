@@ -235,6 +235,11 @@ __device__ __forceinline__ void store_out(const DecodeParams &p, int b, int head
     for (int i = 0; i < p.n_out; ++i) store4<DT>(p.out[i], o, a, bb, c, d);
 }
 
+// this step's merge list (packed upload: right after the work items, offset in the header)
+__device__ __forceinline__ const MergeItem *merges_of(const DecodeParams &p) {
+    return reinterpret_cast<const MergeItem *>(reinterpret_cast<const uint8_t *>(p.hdr) + p.hdr->o_merges);
+}
+
 // ------------------------------------------------------------------ fused append
 // The new token's K and V rows (row b of k_new / v_new, kv head g) as 16-byte
 // chunks: i in [0, 2*CPR): tensor i / CPR (0 = K, 1 = V), chunk cc = i % CPR of
@@ -855,7 +860,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 if (threadIdx.x == 32) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     const int done = atomicAdd(p.merge_counters + it.mg, 1);
-                    const int last = done == p.merges[it.mg].nparts - 1;
+                    const int last = done == merges_of(p)[it.mg].nparts - 1;
                     if (last) {
                         p.merge_counters[it.mg] = 0;            // every split has arrived: re-arm
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 if (k == 0 && threadIdx.x == 32) TRACE(9);
 #endif
                 if (*merge_flag) {
-                    merge_pair<DT, G>(p, p.merges[it.mg], threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
+                    merge_pair<DT, G>(p, merges_of(p)[it.mg], threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
                                       [] { named_bar_sync(1, NC * 32); });
 #ifdef APEX_TRACE
                     named_bar_sync(1, NC * 32);
@@ -895,7 +900,7 @@ __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeP
     asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
     const int n = p.hdr->n_merges;                          // fixed grid, grid-stride over this step's pairs
     for (int i = blockIdx.x; i < n; i += gridDim.x)
-        merge_pair<DT, G>(p, p.merges[i], threadIdx.x, blockDim.x, red, redml, kMergeThreads,
+        merge_pair<DT, G>(p, merges_of(p)[i], threadIdx.x, blockDim.x, red, redml, kMergeThreads,
                           [] { __syncthreads(); });
 }
 

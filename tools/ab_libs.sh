@@ -5,5 +5,5 @@ set -u
 O=$PWD/gpurun_out/ab_libs; mkdir -p $O
 cfgs=$1; shift
 for c in $cfgs; do for r in 1 2; do for v in "$@"; do
-  APEX_LIB=ab/$v.so timeout 600 python bench.py --config $c --no-cpu --no-e2e --steps 10 > $O/${v}_${c}_$(date +%s%N).json 2>/dev/null
+  APEX_LIB=ab/$v.so timeout 600 python bench.py --config $c --no-cpu --steps 10 > $O/${v}_${c}_$(date +%s%N).json 2>/dev/null
 done; done; done
