@@ -529,9 +529,12 @@ def run_apex(args):
                                    "checked": "all-gathered heads" if head_mode else "rank-0 requests"}
     # ---- end-to-end leg: host (pinned) inputs -> C ABI -> host outputs, every step
     if not args.no_e2e:
-        qh = [torch.empty((B, hq, D), dtype=tdt, pin_memory=True) for _ in range(P)]
-        kh = [torch.empty((B, hkv, D), dtype=tdt, pin_memory=True) for _ in range(P)]
-        vh = [torch.empty((B, hkv, D), dtype=tdt, pin_memory=True) for _ in range(P)]
+        # one pinned [q | k | v] buffer per physical layer -> ONE H2D copy per layer-call
+        nq, nk = B * hq * D, B * hkv * D
+        qkvh = [torch.empty((nq + 2 * nk,), dtype=tdt, pin_memory=True) for _ in range(P)]
+        qh = [t[:nq].view(B, hq, D) for t in qkvh]
+        kh = [t[nq:nq + nk].view(B, hkv, D) for t in qkvh]
+        vh = [t[nq + nk:].view(B, hkv, D) for t in qkvh]
         oh = [torch.empty((B, hq, D), dtype=tdt, pin_memory=True) for _ in range(P)]
         qs, ks, vs = inputs[-1]
         for p in range(P):
@@ -541,9 +544,10 @@ def run_apex(args):
         # double-buffered device staging; H2D of layer l+1 and D2H of layer l-1 run on a
         # copy stream underneath layer l's append + decode on the compute stream
         NB = 2
-        qd = [torch.empty_like(qs[0]) for _ in range(NB)]
-        kd = [torch.empty_like(ks[0]) for _ in range(NB)]
-        vd = [torch.empty_like(vs[0]) for _ in range(NB)]
+        qkvd = [torch.empty((nq + 2 * nk,), dtype=tdt, device=dev) for _ in range(NB)]
+        qd = [t[:nq].view(B, hq, D) for t in qkvd]
+        kd = [t[nq:nq + nk].view(B, hkv, D) for t in qkvd]
+        vd = [t[nq + nk:].view(B, hkv, D) for t in qkvd]
         od = [torch.empty_like(qs[0]) for _ in range(NB)]
         # separate H2D and D2H streams: on one in-order copy stream the H2D of layer l+1
         # would queue behind the D2H of layer l, i.e. behind layer l's decode (measured:
@@ -561,9 +565,7 @@ def run_apex(args):
                 p, j = l % P, l % NB
                 with torch.cuda.stream(h2d_s):
                     h2d_s.wait_event(buf_free[j])
-                    qd[j].copy_(qh[p], non_blocking=True)
-                    kd[j].copy_(kh[p], non_blocking=True)
-                    vd[j].copy_(vh[p], non_blocking=True)
+                    qkvd[j].copy_(qkvh[p], non_blocking=True)
                     h2d_done[j].record(h2d_s)
                 comp.wait_event(h2d_done[j])
                 if fused_append:
@@ -611,7 +613,7 @@ def run_apex(args):
         result["e2e"] = {"value": total_tokens / (e_ms * 1e-3), "unit": UNIT,
                          "h2d_bytes_per_step": L * B * (hq + 2 * hkv) * D * es,
                          "d2h_bytes_per_step": L * B * hq * D * es, "ms_per_step": e_ms / K,
-                         "path": "pinned host q/k/v -> H2D on an H2D stream (double-buffered, overlapped with the "
+                         "path": "pinned host [q|k|v] -> one H2D copy per layer on an H2D stream (double-buffered, overlapped with the "
                                  "previous layer) -> PagedKVCache.append/decode (C ABI) -> D2H of out on a D2H "
                                  "stream -> pinned host"}
     if rank == 0:
