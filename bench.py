@@ -1,38 +1,46 @@
 #!/usr/bin/env python
 """Decode-attention benchmark (BASELINE.json metric) -- one JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--mode req|head]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--mode req|head]
                     [--impl apex|reference]
+
+Default workload: C5 (BASELINE.json configs[4], the config the metric's
+"1/2/4/8 B200" is quoted on): LLaMA-3.1-8B GQA, batch 1024, context 16K,
+32 logical layers.  N = 1 serves the whole batch; N > 1 shards ONE global batch
+(strong scaling) -- by default by KV head (--mode head: rank r owns kv heads
+[r*Hkv/N, (r+1)*Hkv/N) and their q-groups, writes its outputs head-major and
+NCCL all-gathers them, overlapped with the next layer: the only collective of
+the path), or by request (--mode req: LPT on context length, no collective).
+Other configs (--config c1..c4) run weak scaling for N > 1 (each rank its own
+batch of the config).
+
+`--gpus N` without WORLD_SIZE in the environment re-launches this script under
+torch.distributed.run with N ranks (the driver's own launch sets WORLD_SIZE and
+is used as is).  If fewer than N GPUs are visible the ranks share GPU 0 over
+gloo (a logic check of the sharded path: its throughput is meaningless and the
+line says so in config.devices).
 
 A step is one pass of the whole hot path over one batch:
 apex_kv_alloc (+1 token per request; planner + metadata upload) and, for each of
-the L logical layers, the KV append + decode attention (+ the LSE merge) -- by
-default in one launch (apex_decode_attention_append; --append separate runs
-apex_kv_append + apex_decode_attention).
-value = decode tokens/s of the whole job (one token per request per step needs
-all L layers) = sum_ranks(B_r) * K / max_ranks(time of K steps).
+the L logical layers, the KV append + decode attention (+ the LSE merge)
+[+ the head all-gather].  value = decode tokens/s of the whole job (one token
+per request per step needs all L layers) = global batch * K / max_ranks(time).
 
 Inputs are synthetic (synth/, seeded), resident in HBM before the timed region.
-When the KV of all physical layers streams >> L2 (126 MB) per step (c2..c5) no
-L2 flush is needed; otherwise (c1: 17 MB) a 512 MiB buffer is written before
-every step, outside that step's timing events, and the time is the sum of the
-per-step event intervals.  KV pools
-exist for P physical layers; logical layer l uses physical pool l % P (P = L
-whenever the 32 layers fit, e.g. the default c3).  For N > 1 the driver
-launches one process per GPU via torch.distributed.run; requests are
-partitioned across ranks (weak scaling: each rank serves its own batch of the
-config) with no data-path collective; --config c5 shards one global batch
-(strong scaling; --mode head adds the NCCL all-gather of head-sharded outputs).
+KV pools exist for P physical layers; logical layer l uses pool l % P.  When a
+layer-call streams >> L2 (126 MB) no flush is needed; otherwise (c1: 17 MB) a
+512 MiB buffer is written before every step, outside that step's timing events.
 
 --impl reference times the float64 oracle (oracle/, the method's plain
 definition) on this box's host cores on a bounded sample of the same workload
-and extrapolates to the same metric.
+and extrapolates to the same metric (rank 0 only; other ranks exit at once).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -50,34 +58,37 @@ from synth import TENSOR_K, TENSOR_Q, TENSOR_V, WORKLOADS  # noqa: E402
 METRIC = "decode-attention tokens/s and achieved HBM GB/s vs ~8 TB/s at 1/2/4/8 B200"
 UNIT = "tokens/s"
 FALLBACK_HBM_GBS = 6650.0
+L2_BYTES_B200 = 126.5 * 2 ** 20       # L2 of one B200 (cudaDeviceProp.l2CacheSize on the box: 126.5 MiB)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["apex", "reference"], default="apex")
-    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
-    ap.add_argument("--mode", choices=["req", "head"], default="req")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c5")
+    ap.add_argument("--mode", choices=["req", "head"], default=None,
+                    help="c5 sharding for N > 1 (default head: the NCCL all-gather path)")
     ap.add_argument("--phys-layers", type=int, default=0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--out", default="")
     ap.add_argument("--append", choices=["fused", "separate"], default="fused",
-                    help="fused: apex_decode_attention_append (append inside the decode launch); "
-                         "separate: apex_kv_append + apex_decode_attention")
+                    help="fused: apex_decode_attention_append (append inside the decode launch in the latency "
+                         "regime); separate: apex_kv_append + apex_decode_attention")
     ap.add_argument("--sched", type=int, default=None,
                     help="planner schedule override (apex_kv_set_sched): -2 guided (library default), "
                          "-1 uniform dynamic split, 0..1000 stream-K")
     ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
-                    help="head mode: NCCL all_gather_into_tensor, or stores into peers' symmetric memory "
-                         "from the decode epilogue (experimental, needs >= 2 GPUs)")
-    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
-                    help="gloo + APEX_BENCH_SAME_DEVICE=1 runs several ranks on one GPU (logic test only)")
-    return ap.parse_args()
+                    help="head mode: NCCL all_gather_into_tensor on head-major slices (overlapped with the next "
+                         "layer), or stores into peers' symmetric memory from the decode epilogue with in-kernel "
+                         "completion flags (needs >= N GPUs)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default=None,
+                    help="default nccl; gloo when the ranks share one GPU (logic check)")
+    return ap.parse_args(argv)
 
 
 # ------------------------------------------------------------------ helpers
@@ -91,11 +102,12 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback 6.65 TB/s from B200_PROFILING.md (MEASURED_PEAKS.json absent)"
 
 
-def ncu_traffic(config: str):
-    """dram bytes/launch of the decode kernel from the committed ncu --set full summary, if any."""
+def ncu_traffic(config: str, mode: str, world: int):
+    """dram bytes/launch of the decode kernel from the committed ncu --set full summary for
+    exactly this (config, sharding mode, N), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f)[config]["decode_dram_bytes_per_launch"]
+            return json.load(f)[f"{config}:{mode}:{world}"]["decode_dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -166,7 +178,17 @@ def cpu_cores():
     return len(os.sched_getaffinity(0))
 
 
+def same_device_ranks() -> bool:
+    return os.environ.get("APEX_BENCH_SAME_DEVICE") == "1"
+
+
 # ------------------------------------------------------------------ workload layout
+
+def resolve_mode(w, world, mode):
+    if w.name != "c5":
+        return "req"
+    return mode or ("head" if world > 1 else "req")
+
 
 def rank_workload(w, rank, world, mode):
     """Requests (global ids), contexts at the first step and head slice of this rank."""
@@ -176,16 +198,38 @@ def rank_workload(w, rank, world, mode):
         ids = np.arange(rank * w.batch, (rank + 1) * w.batch)
         ctx = w.contexts(w.batch, b0=rank * w.batch) if w.ctx_kind == "hash" else w.contexts(w.batch)
         return dict(ids=ids, ctx=ctx, hq=hq, hkv=hkv, q_off=0, kv_off=0, scaling="weak",
-                    global_batch=w.batch * world, parallelism=f"req{world}")
+                    global_batch=w.batch * world, parallelism=f"req{world}" if world > 1 else "single")
     from paper_2506_03296_b200.sharding import head_range, lpt_partition
     ctx_all = w.contexts()
-    if mode == "req":
+    par = "single" if world == 1 else f"{mode}{world}"
+    if mode == "req" or world == 1:
         part = lpt_partition(ctx_all, world)[rank]
         return dict(ids=np.asarray(part), ctx=ctx_all[part], hq=hq, hkv=hkv, q_off=0, kv_off=0,
-                    scaling="strong", global_batch=w.batch, parallelism=f"req{world}")
+                    scaling="strong", global_batch=w.batch, parallelism=par)
     kv_lo, kv_hi, q_lo, q_hi = head_range(hkv, hq, rank, world)
     return dict(ids=np.arange(w.batch), ctx=ctx_all, hq=q_hi - q_lo, hkv=kv_hi - kv_lo, q_off=q_lo, kv_off=kv_lo,
-                scaling="strong", global_batch=w.batch, parallelism=f"head{world}")
+                scaling="strong", global_batch=w.batch, parallelism=par)
+
+
+def l2_policy(w, wl):
+    """(flush?, text) from the rank's per-layer-call KV bytes vs the 126.5 MiB L2."""
+    es = elem_bytes(w.dtype)
+    call = alg_bytes(wl["ctx"], wl["hkv"], wl["hq"], w.head_dim, es)
+    if call >= 4 * L2_BYTES_B200:
+        return False, f"no flush: every layer-call streams {call / 2 ** 30:.2f} GiB of KV per GPU >> 126.5 MiB L2"
+    return True, (f"flushed: a layer-call streams {call / 2 ** 20:.1f} MiB of KV, within reach of the 126.5 MiB L2, "
+                  "so a 512 MiB buffer is written before every step (outside the per-step events; "
+                  "time = sum of per-step intervals)")
+
+
+def bench_config(w, wl, world, mode):
+    """`config` of the JSON line -- identical in the apex and the reference arm."""
+    ctx0 = np.asarray(wl["ctx"], dtype=np.int64)
+    return {"workload": f"{w.name}: {w.desc}", "global_batch": int(wl["global_batch"]), "layers": w.layers,
+            "num_q_heads": w.num_q_heads, "num_kv_heads": w.num_kv_heads, "head_dim": w.head_dim,
+            "block_size": 16, "kv_dtype": w.dtype,
+            "ctx_first_step": {"min": int(ctx0.min()), "mean": float(ctx0.mean()), "max": int(ctx0.max())},
+            "parallelism": wl["parallelism"], "l2": l2_policy(w, wl)[1]}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -213,12 +257,12 @@ class OracleSampler:
                                         self.seed, head_offset=wl["kv_off"]))
         return self.kv[i]
 
-    def run(self, ctx_now, seconds, max_requests=12):
+    def run(self, ctx_now, seconds, max_requests=12, nthreads=None):
         """Oracle passes over the first `max_requests` sampled requests until `seconds` of
         oracle time (at least one request).  Returns (rate in (token x q-head)/s, oracle
-        seconds, {request index: out [Hq][D]})."""
+        seconds, {request index: out [Hq][D]}, kv tokens processed)."""
         from oracle import attention as oa
-        t_or, work, outs = 0.0, 0, {}
+        t_or, work, kv_tok, outs = 0.0, 0, 0, {}
         sample = self.order[:max_requests]
         for j in range(1 << 20):
             i = sample[j % len(sample)]
@@ -227,19 +271,20 @@ class OracleSampler:
             q = synth.gen_rows(TENSOR_Q, self.layer, [int(wl["ids"][i])], [n - 1], wl["hq"], self.w.head_dim,
                                self.dtype, self.seed, head_offset=wl["q_off"])
             t0 = time.perf_counter()
-            out = oa.decode_attention(q, [k[:n]], [v[:n]], self.dtype, nthreads=self.cores)
+            out = oa.decode_attention(q, [k[:n]], [v[:n]], self.dtype, nthreads=nthreads or self.cores)
             t_or += time.perf_counter() - t0
             work += n * wl["hq"]
+            kv_tok += n
             outs[i] = out[0]
             if t_or >= seconds:
                 break
-        return work / t_or, t_or, outs
+        return work / t_or, t_or, outs, kv_tok
 
-    def describe(self, outs, ctx_now, n_req):
+    def describe(self, outs, ctx_now, n_req, threads=None):
         ctxs = sorted(int(ctx_now[i]) for i in outs)
         return (f"{len(outs)} whole requests (ctx {ctxs[:6]}{'...' if len(ctxs) > 6 else ''}), all "
-                f"{self.wl['hq']} q-heads, 1 layer; float64 C oracle on {self.cores} threads; extrapolated "
-                f"linearly in (tokens x heads) to {n_req} requests x {self.w.layers} layers")
+                f"{self.wl['hq']} q-heads, 1 layer; float64 C oracle on {threads or self.cores} threads; "
+                f"extrapolated linearly in (tokens x heads) to {n_req} requests x {self.w.layers} layers")
 
 
 # ------------------------------------------------------------------ reference arm
@@ -249,15 +294,18 @@ def run_reference(args):
     if rank != 0:
         return
     w = WORKLOADS[args.config]
-    wl = rank_workload(w, 0, 1, args.mode)          # the host's CPU serves the whole batch
+    mode = resolve_mode(w, world, args.mode)
+    wl_cfg = rank_workload(w, 0, world, mode)       # the apex arm's rank-0 view: same config dict
+    wl = rank_workload(w, 0, 1, "req")              # the host's CPU serves the whole batch
     ctx = np.asarray(wl["ctx"], dtype=np.int64)
     S = args.warmup + args.steps
     sampler = OracleSampler(w, wl, 0, args.seed, w.dtype, ctx + S)
     per_step = max(0.5, 30.0 / max(S, 1))           # bounded: ~30 s of oracle time for the whole run
-    rates, step_s_list, desc = [], [], ""
+    rates, step_s_list, desc, t_total = [], [], "", 0.0
     for s in range(S):
         ctx_s = ctx + s
-        rate, _, outs = sampler.run(ctx_s, per_step)
+        rate, t_or, outs, _ = sampler.run(ctx_s, per_step)
+        t_total += t_or
         if s >= args.warmup:
             rates.append(rate)
             step_s_list.append(float((ctx_s * wl["hq"]).sum()) * w.layers / rate)
@@ -265,12 +313,13 @@ def run_reference(args):
     cores = sampler.cores
     step_s = statistics.median(step_s_list)
     value = len(ctx) / step_s       # tokens/s of one host; unchanged by how many GPUs the apex arm uses
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
-            "config": {"workload": f"{w.name}: {w.desc}", "global_batch": wl["global_batch"], "layers": w.layers,
-                       "num_q_heads": w.num_q_heads, "num_kv_heads": w.num_kv_heads, "head_dim": w.head_dim,
-                       "kv_dtype": w.dtype},
+            "scaling": wl_cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+            "config": bench_config(w, wl_cfg, world, mode),
+            # the oracle is timed on a bounded sample of each step and extrapolated to the
+            # whole step: ms_per_step is NOT a measured wall time of one full step
+            "extrapolated": True, "oracle_seconds_measured": t_total,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"per step: {desc}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -286,11 +335,15 @@ def run_apex(args):
     from paper_2506_03296_b200.kvcache import PagedKVCache, synth_rows, torch_dtype
 
     rank, world, local = dist_env()
-    if os.environ.get("APEX_BENCH_SAME_DEVICE") == "1":
-        local = 0                                     # test mode: several ranks share GPU 0 (gloo only)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    shared = same_device_ranks()
+    if shared:
+        local = 0                                     # ranks share GPU 0 (gloo only; logic check)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    gloo = args.dist_backend == "gloo"
+    backend = args.dist_backend or ("gloo" if shared else "nccl")
+    gloo = backend == "gloo"
     if world > 1:
         if gloo:
             dist.init_process_group("gloo")
@@ -298,18 +351,25 @@ def run_apex(args):
             dist.init_process_group("nccl", device_id=dev)
     coll_dev = torch.device("cpu") if gloo else dev   # where small reduction tensors live
     w = WORKLOADS[args.config]
-    wl = rank_workload(w, rank, world, args.mode)
+    mode = resolve_mode(w, world, args.mode)
+    wl = rank_workload(w, rank, world, mode)
     ids, ctx0 = wl["ids"], np.asarray(wl["ctx"], dtype=np.int64)
     B, hq, hkv, D, L, dt = len(ids), wl["hq"], wl["hkv"], w.head_dim, w.layers, w.dtype
     es = elem_bytes(dt)
     tdt = torch_dtype(dt)
     W, K = args.warmup, args.steps
+    head_mode = wl["parallelism"].startswith("head")
+    fused = head_mode and args.gather == "fused"
+    if fused and (gloo or shared):
+        raise SystemExit("--gather fused needs one GPU per rank (peer-mapped symmetric memory)")
     n_steps_total = 2 * (W + K) + 1                 # value leg + e2e leg
     max_len = int(ctx0.max()) + n_steps_total + 1
     mbps = -(-max_len // 16)
     blocks_per_layer = int(sum(-(-(int(c) + n_steps_total) // 16) for c in ctx0)) + 16
     layer_bytes = blocks_per_layer * hkv * 16 * D * es * 2
     free, _ = torch.cuda.mem_get_info(dev)
+    if shared:
+        free //= world                                # the ranks split one GPU's memory
     chunk_rows = 1 << 19
     reserve = 6 * 2 ** 30 + 4 * chunk_rows * max(hkv, 1) * D * es
     P = args.phys_layers or max(1, min(L, int((free - reserve) * 0.95) // layer_bytes))
@@ -360,51 +420,78 @@ def run_apex(args):
 
     inputs = [step_inputs(s) for s in range(W + K)]
     outs = [torch.empty((B, hq, D), dtype=tdt, device=dev) for _ in range(P)]
-    gathered = [None] * P
-    head_mode = w.name == "c5" and args.mode == "head" and world > 1
-    fused = head_mode and args.gather == "fused"
-    fused_append = args.append == "fused" and not fused      # the symmetric-memory epilogue uses the _ex call
-    if head_mode:
-        from paper_2506_03296_b200.sharding import gather_heads
+    comp = torch.cuda.current_stream(dev)
+    hg = sg = None
+    if head_mode and not fused:
+        # head-major [Hq/N][B][D] slices, all-gathered into [Hq][B][D] (no permute) on
+        # NCCL's stream while the next layer decodes
+        from paper_2506_03296_b200.sharding import HeadGather
+        hg = HeadGather(hq, B, D, tdt, dev, nbuf=2, backend="gloo" if gloo else "nccl")
     if fused:
-        # all-gather fused into the decode epilogue: every rank stores its head slice
-        # into all ranks' symmetric buffers (peer-mapped over NVLink); experimental
-        from paper_2506_03296_b200 import apex as A
-        from paper_2506_03296_b200.sharding import symmetric_output
-        symm = [symmetric_output((B, w.num_q_heads, D), tdt, dev) for _ in range(P)]
+        from paper_2506_03296_b200.sharding import SignalledGather, symmetric_output
+        NBUF = 2
+        bufs, sigs = [], []
+        for _ in range(NBUF):
+            t, h = symmetric_output((w.num_q_heads, B, D), tdt, dev)
+            s_t, s_h = symmetric_output((2, world), torch.int32, dev)
+            s_t.zero_()
+            bufs.append((t, h))
+            sigs.append((s_t, s_h))
+        torch.cuda.synchronize()
+        dist.barrier()
+        ptrs = [list(h.buffer_ptrs) for _, h in bufs]
+        ready = [[int(p) for p in h.buffer_ptrs] for _, h in sigs]                 # row 0 of [2][world]
+        freep = [[int(p) + 4 * world for p in h.buffer_ptrs] for _, h in sigs]     # row 1
+        sg = SignalledGather(rank, world, ptrs, ready, freep)
+        reader = torch.cuda.Stream(dev)
+        sig_status = torch.zeros(1, dtype=torch.int32, device=dev)
+        epoch = [0]
+    fused_append = args.append == "fused" and not head_mode   # the _ex epilogue has no append variant
     ones = [1] * B
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K * L)]
-    # L2: every step streams the KV of P physical layers; if that is not >> L2, flush
-    # L2 before each step (outside the step's events) so every read comes from HBM
-    step_kv_bytes = P * alg_bytes(ctx0, hkv, hq, D, es)
-    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if step_kv_bytes < 4 * l2_bytes else None
+    flush, _ = l2_policy(w, wl)
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    gathered = {}
 
     def step(s, timed_idx=None):
         qs, ks, vs = inputs[s]
         cache.alloc(seq, ones)
         for l in range(L):
-            p = l % P
+            p, j = l % P, l % 2
             if not fused_append:
                 cache.append(p, ks[p], vs[p])
+            if hg is not None:
+                dst = hg.local(j)                     # WAR: the gather of layer l-2 has read it
             if timed_idx is not None:
                 ev[timed_idx * L + l][0].record()
             if fused_append:
                 cache.decode_append(p, qs[p], ks[p], vs[p], out=outs[p])
-            elif fused:
-                buf, hdl = symm[p]
-                A.apex_decode_attention_ex(cache.handle, p, qs[p].data_ptr(), list(hdl.buffer_ptrs),
-                                           w.num_q_heads * D, wl["q_off"], 1.0 / D ** 0.5,
-                                           torch.cuda.current_stream(dev).cuda_stream)
-                hdl.barrier(channel=0)               # remote slices landed before anyone reads buf
-                gathered[p] = buf
+            elif hg is not None:
+                cache.decode_into(p, qs[p], [dst], layout="hbd")
+            elif sg is not None:
+                epoch[0] += 1
+                jj = sg.decode(cache, p, qs[p], epoch[0], w.num_q_heads, sig_status.data_ptr())
             else:
                 cache.decode(p, qs[p], out=outs[p])
             if timed_idx is not None:
                 ev[timed_idx * L + l][1].record()
-            if head_mode and not fused:
-                gathered[p] = gather_heads(outs[p]) if not gloo else gather_heads(outs[p].cpu())
+            if hg is not None:
+                hg.start(j)                           # returns at once; overlaps layer l+1
+            elif sg is not None:
+                e = torch.cuda.Event()
+                e.record(comp)
+                reader.wait_event(e)
+                sg.wait_ready(jj, epoch[0], reader.cuda_stream, sig_status.data_ptr())
+                sg.release(jj, epoch[0], reader.cuda_stream)
+        # the step ends when the last gathers have landed
+        if hg is not None:
+            for j in range(2):
+                gathered[j] = hg.result(j)
+        elif sg is not None:
+            e = torch.cuda.Event()
+            e.record(reader)
+            comp.wait_event(e)
 
     def barrier():
         if world > 1:
@@ -422,8 +509,8 @@ def run_apex(args):
     n_items, n_merges = len(cache.plan()[0]), cache.plan()[1]
     decode_launches = cache.decode_launches()
     clocks = ClockSampler(local) if rank == 0 else None
-    barrier()
     torch.cuda.synchronize()
+    barrier()
     if clocks:
         clocks.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -452,54 +539,55 @@ def run_apex(args):
     bytes_per_launch = float(np.mean([alg_bytes(c, hkv, hq, D, es) for c in ctx_steps]))
     achieved_gbs = bytes_per_launch / (avg_launch_us * 1e-6) / 1e9
     peak, peak_src = measured_peak()
-    total_tokens = B * K
-    if world > 1:
-        tt = torch.tensor([float(B * K)], dtype=torch.float64, device=coll_dev)
-        if wl["parallelism"].startswith("head"):
-            tt /= world                               # every rank serves the same requests
-        dist.all_reduce(tt)
-        total_tokens = float(tt.item())
+    total_tokens = float(wl["global_batch"] * K) if w.name == "c5" else float(B * K * world)
     value = total_tokens / (t_ms * 1e-3)
     step_bytes = L * bytes_per_launch
+    ctx_mean_timed = float(np.mean([c.mean() for c in ctx_steps]))
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
               "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
               "dtype": dt, "data": "synthetic (seeded splitmix64/lowbias32 generator, on-device twin)",
-              "config": {"workload": f"{w.name}: {w.desc}", "global_batch": wl["global_batch"],
-                         "batch_per_gpu": B, "layers": L, "phys_layers": P, "num_q_heads": w.num_q_heads,
-                         "num_kv_heads": w.num_kv_heads, "head_dim": D, "block_size": 16,
-                         "ctx_first_step": {"min": int(ctx0.min()), "mean": float(ctx0.mean()),
-                                            "max": int(ctx0.max())},
-                         "parallelism": wl["parallelism"] + ("+fused_gather" if fused else ""),
-                         "l2": (f"no flush: each step streams {step_kv_bytes / 2**30:.2f} GiB of KV >> "
-                                f"{l2_bytes / 2**20:.0f} MiB L2" if flush_buf is None else
-                                f"flushed: {step_kv_bytes / 2**20:.1f} MiB of KV per step fits the "
-                                f"{l2_bytes / 2**20:.0f} MiB L2, so a 512 MiB buffer is written before every "
-                                "step (outside the per-step events; time = sum of per-step intervals)"),
-                         "work_items_per_layer": n_items, "split_merges_per_layer": n_merges,
-                         "append": ("apex_decode_attention_append (latency regime: inside the decode launch; "
-                                    "bandwidth regime: append kernel + decode kernel)") if fused_append
-                                   else "separate apex_kv_append launch"},
-              "hbm_gbs_step": step_bytes / (t_ms / K * 1e-3) / 1e9,
+              "config": bench_config(w, wl, world, mode),
+              "details": {"batch_per_gpu": B, "q_heads_per_gpu": hq, "kv_heads_per_gpu": hkv, "phys_layers": P,
+                          "devices": "ranks share GPU 0 (gloo): logic check, throughput not meaningful"
+                          if shared and world > 1 else f"{world} GPU(s), one rank each",
+                          "dist_backend": backend if world > 1 else None,
+                          "gather": (("fused epilogue stores + in-kernel completion flags" if fused else
+                                      f"{backend} all_gather_into_tensor of head-major slices, async, overlapped "
+                                      "with the next layer") if head_mode else None),
+                          "work_items_per_layer": n_items, "split_merges_per_layer": n_merges,
+                          "decode_launches_per_call": decode_launches,
+                          "append": ("apex_decode_attention_append (latency regime: inside the decode launch; "
+                                     "bandwidth regime: append kernel + decode kernel)") if fused_append
+                          else "separate apex_kv_append launch"},
+              "hbm_gbs_step_per_gpu": step_bytes / (t_local / K * 1e-3) / 1e9,
               "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                           "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.config),
+                           "frac": achieved_gbs / peak, "traffic": ncu_traffic(w.name, mode, world),
                            "kernel": "apex_decode_attention = apex_decode_kernel (+ apex_merge_kernel when split "
                                      "pairs are merged in a second launch)",
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
                            "frac_of_8000_gbs": achieved_gbs / 8000.0},
-              # deltas + L x ([append,] decode[, merge]); the append rides in the decode launch only
-              # in the latency regime (decode_launches == 1)
-              "gpu_launches": K * (1 + L * ((0 if fused_append and decode_launches == 1 else 1) + decode_launches)),
+              # ours only (NCCL's kernels excluded): deltas + L x ([append,] decode[, merge])
+              # [+ 2 signal kernels per layer with the fused gather]; the append rides in the
+              # decode launch only in the latency regime (decode_launches == 1)
+              "gpu_launches": K * (1 + L * ((0 if fused_append and decode_launches == 1 else 1) + decode_launches
+                                            + (2 if fused else 0))),
               "prefill_s": t_fill}
     if clk:
         result["clocks"] = clk
 
-    # ---- sampled parity + CPU oracle baseline (rank 0, N = 1)
+    # ---- time prediction (a8) and its online recalibration (f2) at this operating point
+    try:
+        result["cost_model"] = cost_model_check(w, wl, ctx_mean_timed, avg_launch_us, hq, hkv)
+    except Exception as e:  # the table is a committed profile; its absence is reported, not fatal
+        result["cost_model"] = {"error": str(e)}
+
+    # ---- sampled parity + CPU oracle baseline (rank 0)
+    p_last = (L - 1) % P
+    ctx_now = ctx0 + (W + K - 1)                      # context of the last timed step
     if rank == 0 and world == 1 and not args.no_cpu:
-        p_last = (L - 1) % P
-        ctx_now = ctx0 + (W + K - 1)                  # context of the last timed step
         sampler = OracleSampler(w, wl, p_last, args.seed, dt, ctx_now)
-        rate, t_or, o_ref = sampler.run(ctx_now, args.cpu_seconds)
+        rate, t_or, o_ref, kv_tok = sampler.run(ctx_now, args.cpu_seconds)
         cores, desc = sampler.cores, sampler.describe(o_ref, ctx_now, B)
         # the oracle timing above uses the q of the last step: compare with the GPU rows
         got = outs[p_last].to(torch.float64).cpu().numpy()
@@ -508,114 +596,51 @@ def run_apex(args):
         result["parity_sample"] = {"requests": sorted(int(i) for i in o_ref), "rows": len(o_ref) * hq,
                                    "max_abs_err": max(errs), "max_row_normwise_err": max(rel),
                                    "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)"}
+        # single-thread oracle on the same requests (bounded), for the per-core rate
+        rate1, t1s, _, kv_tok1 = sampler.run(ctx_now, min(4.0, args.cpu_seconds / 2), max_requests=1, nthreads=1)
         full_rows = float((ctx_now * hq).sum()) * L
         cpu_tok_s = B / (full_rows / rate)
+        kv_tok_bytes = hkv * D * 2 * es                  # K+V bytes of one cached token (one layer)
+        # N_G / N_C (reading c15): attention rates in kv tokens per us at
+        # this operating point; GPU from the measured layer-call, CPU from the oracle
+        n_g = float(ctx_now.sum()) / avg_launch_us
+        n_c = (kv_tok / t_or) * 1e-6
         result["cpu_baseline"] = {"value": cpu_tok_s, "unit": UNIT, "cores": cores, "kind": "oracle",
                                   "sample": desc, "oracle_seconds": t_or,
+                                  "single_thread": {"value": B / (full_rows / rate1), "unit": UNIT, "cores": 1,
+                                                    "oracle_seconds": t1s,
+                                                    "kv_gbs": kv_tok1 * kv_tok_bytes / t1s / 1e9},
+                                  "kv_gbs": kv_tok * kv_tok_bytes / t_or / 1e9,
+                                  "n_g_tokens_per_us": n_g, "n_c_tokens_per_us": n_c, "n_g_over_n_c": n_g / n_c,
                                   "cpu": _cpu_model()}
     elif rank == 0 and world > 1 and not args.no_cpu:
         # sampled parity of this rank's rows (request sharding) or of the all-gathered
         # full-head output (head sharding) against the oracle over all global heads
-        p_last = (L - 1) % P
-        ctx_now = ctx0 + (W + K - 1)
         full_wl = dict(wl, hq=w.num_q_heads, hkv=w.num_kv_heads, q_off=0, kv_off=0)
         sampler = OracleSampler(w, full_wl, p_last, args.seed, dt, ctx_now)
-        _, _, o_ref = sampler.run(ctx_now, 0.0, max_requests=2)
-        got_t = gathered[p_last] if head_mode else outs[p_last]
+        _, _, o_ref, _ = sampler.run(ctx_now, 0.0, max_requests=2)
+        if hg is not None:
+            got_t = gathered[(L - 1) % 2].permute(1, 0, 2)       # [Hq][B][D] -> [B][Hq][D]
+        elif sg is not None:
+            torch.cuda.synchronize()
+            got_t = bufs[epoch[0] % 2][0].permute(1, 0, 2)       # the last layer-call's buffer
+            result["details"]["signal_timeouts"] = int(sig_status.item())
+        else:
+            got_t = outs[p_last]
         got = got_t.to(torch.float64).cpu().numpy()
         errs = [float(np.abs(got[i] - o_ref[i]).max()) for i in o_ref]
         result["parity_sample"] = {"requests": sorted(int(wl["ids"][i]) for i in o_ref),
                                    "rows": len(o_ref) * w.num_q_heads, "max_abs_err": max(errs),
-                                   "checked": "all-gathered heads" if head_mode else "rank-0 requests"}
+                                   "checked": "all-gathered heads" if head_mode else "rank-0 requests",
+                                   "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)"}
     # ---- end-to-end leg: host (pinned) inputs -> C ABI -> host outputs, every step
     if not args.no_e2e:
-        # one pinned [q | k | v] buffer per physical layer -> ONE H2D copy per layer-call
-        nq, nk = B * hq * D, B * hkv * D
-        qkvh = [torch.empty((nq + 2 * nk,), dtype=tdt, pin_memory=True) for _ in range(P)]
-        qh = [t[:nq].view(B, hq, D) for t in qkvh]
-        kh = [t[nq:nq + nk].view(B, hkv, D) for t in qkvh]
-        vh = [t[nq + nk:].view(B, hkv, D) for t in qkvh]
-        oh = [torch.empty((B, hq, D), dtype=tdt, pin_memory=True) for _ in range(P)]
-        qs, ks, vs = inputs[-1]
-        for p in range(P):
-            qh[p].copy_(qs[p])
-            kh[p].copy_(ks[p])
-            vh[p].copy_(vs[p])
-        # double-buffered device staging; H2D of layer l+1 and D2H of layer l-1 run on a
-        # copy stream underneath layer l's append + decode on the compute stream
-        NB = 2
-        qkvd = [torch.empty((nq + 2 * nk,), dtype=tdt, device=dev) for _ in range(NB)]
-        qd = [t[:nq].view(B, hq, D) for t in qkvd]
-        kd = [t[nq:nq + nk].view(B, hkv, D) for t in qkvd]
-        vd = [t[nq + nk:].view(B, hkv, D) for t in qkvd]
-        od = [torch.empty_like(qs[0]) for _ in range(NB)]
-        # separate H2D and D2H streams: on one in-order copy stream the H2D of layer l+1
-        # would queue behind the D2H of layer l, i.e. behind layer l's decode (measured:
-        # no overlap at all, tools/e2e_probe.py)
-        comp, h2d_s, d2h_s = torch.cuda.current_stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        h2d_done = [torch.cuda.Event() for _ in range(NB)]
-        dec_done = [torch.cuda.Event() for _ in range(NB)]
-        buf_free = [torch.cuda.Event() for _ in range(NB)]
-        for e in buf_free:
-            e.record(comp)
-
-        def e2e_step():
-            cache.alloc(seq, ones)
-            for l in range(L):
-                p, j = l % P, l % NB
-                with torch.cuda.stream(h2d_s):
-                    h2d_s.wait_event(buf_free[j])
-                    qkvd[j].copy_(qkvh[p], non_blocking=True)
-                    h2d_done[j].record(h2d_s)
-                comp.wait_event(h2d_done[j])
-                if fused_append:
-                    cache.decode_append(p, qd[j], kd[j], vd[j], out=od[j])
-                else:
-                    cache.append(p, kd[j], vd[j])
-                    cache.decode(p, qd[j], out=od[j])
-                if head_mode:
-                    oh[p] = gather_heads(od[j] if not gloo else od[j].cpu()).cpu()
-                    buf_free[j].record(comp)
-                    continue
-                dec_done[j].record(comp)
-                with torch.cuda.stream(d2h_s):
-                    d2h_s.wait_event(dec_done[j])
-                    oh[p].copy_(od[j], non_blocking=True)
-                    buf_free[j].record(d2h_s)
-
-        for _ in range(W):
-            e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if flush_buf is None:
-            a.record(comp)
-            for _ in range(K):
-                e2e_step()
-            for e in buf_free:                     # the last D2H copies are inside the timed region
-                comp.wait_event(e)
-            b.record(comp)
-            torch.cuda.synchronize()
-            e_local = a.elapsed_time(b)
-        else:
-            e_local = 0.0
-            for k in range(K):                     # flush, then one step with its copies
-                flush_buf.fill_(k & 0xff)
-                a.record(comp)
-                e2e_step()
-                for e in buf_free:
-                    comp.wait_event(e)
-                b.record(comp)
-                torch.cuda.synchronize()
-                e_local += a.elapsed_time(b)
-        barrier()
-        e_ms = max_over_ranks(e_local)
-        result["e2e"] = {"value": total_tokens / (e_ms * 1e-3), "unit": UNIT,
-                         "h2d_bytes_per_step": L * B * (hq + 2 * hkv) * D * es,
-                         "d2h_bytes_per_step": L * B * hq * D * es, "ms_per_step": e_ms / K,
-                         "path": "pinned host [q|k|v] -> one H2D copy per layer on an H2D stream (double-buffered, overlapped with the "
-                                 "previous layer) -> PagedKVCache.append/decode (C ABI) -> D2H of out on a D2H "
-                                 "stream -> pinned host"}
+        e2e = run_e2e(args, cache, inputs, seq, B, hq, hkv, D, L, P, tdt, dev, hg, fused_append, flush_buf,
+                      barrier, max_over_ranks, K, W, total_tokens, es, world, head_mode, w)
+        if e2e:
+            result["e2e"] = e2e
+    if hg is not None:
+        hg.close()
     if rank == 0:
         line = json.dumps(result)
         print(line, flush=True)
@@ -623,7 +648,137 @@ def run_apex(args):
             with open(args.out, "a") as f:
                 f.write(line + "\n")
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def run_e2e(args, cache, inputs, seq, B, hq, hkv, D, L, P, tdt, dev, hg, fused_append, flush_buf, barrier,
+            max_over_ranks, K, W, total_tokens, es, world, head_mode, w):
+    import torch
+    if args.gather == "fused" and head_mode:
+        return None                                   # the symmetric-memory variant has no e2e leg
+    # one pinned [q | k | v] buffer per physical layer -> ONE H2D copy per layer-call
+    nq, nk = B * hq * D, B * hkv * D
+    qkvh = [torch.empty((nq + 2 * nk,), dtype=tdt, pin_memory=True) for _ in range(P)]
+    qh = [t[:nq].view(B, hq, D) for t in qkvh]
+    kh = [t[nq:nq + nk].view(B, hkv, D) for t in qkvh]
+    vh = [t[nq + nk:].view(B, hkv, D) for t in qkvh]
+    h_out = w.num_q_heads if head_mode else hq        # head mode: every rank reads the gathered heads
+    oh = [torch.empty((h_out, B, D) if head_mode else (B, hq, D), dtype=tdt, pin_memory=True) for _ in range(P)]
+    qs, ks, vs = inputs[-1]
+    for p in range(P):
+        qh[p].copy_(qs[p])
+        kh[p].copy_(ks[p])
+        vh[p].copy_(vs[p])
+    # double-buffered device staging; H2D of layer l+1 and D2H of layer l-1 run on copy
+    # streams underneath layer l's append + decode on the compute stream (separate H2D
+    # and D2H streams: on one in-order copy stream the H2D of layer l+1 would queue
+    # behind the D2H of layer l, i.e. behind layer l's decode)
+    NB = 2
+    qkvd = [torch.empty((nq + 2 * nk,), dtype=tdt, device=dev) for _ in range(NB)]
+    qd = [t[:nq].view(B, hq, D) for t in qkvd]
+    kd = [t[nq:nq + nk].view(B, hkv, D) for t in qkvd]
+    vd = [t[nq + nk:].view(B, hkv, D) for t in qkvd]
+    od = [torch.empty_like(qs[0]) for _ in range(NB)]
+    comp, h2d_s, d2h_s = torch.cuda.current_stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    h2d_done = [torch.cuda.Event() for _ in range(NB)]
+    dec_done = [torch.cuda.Event() for _ in range(NB)]
+    buf_free = [torch.cuda.Event() for _ in range(NB)]
+    for e in buf_free:
+        e.record(comp)
+
+    def e2e_step():
+        cache.alloc(seq, [1] * B)
+        for l in range(L):
+            p, j = l % P, l % NB
+            with torch.cuda.stream(h2d_s):
+                h2d_s.wait_event(buf_free[j])
+                qkvd[j].copy_(qkvh[p], non_blocking=True)
+                h2d_done[j].record(h2d_s)
+            comp.wait_event(h2d_done[j])
+            if head_mode:
+                cache.append(p, kd[j], vd[j])
+                dst = hg.local(j)
+                cache.decode_into(p, qd[j], [dst], layout="hbd")
+                hg.start(j)
+                buf_free[j].record(comp)              # q/k/v staging consumed by the decode
+                with torch.cuda.stream(d2h_s):
+                    full = hg.result(j)               # the D2H stream waits for the gather
+                    oh[p].copy_(full, non_blocking=True)
+                    hg.release(j)                     # the next gather into this buffer waits for the copy
+                continue
+            if fused_append:
+                cache.decode_append(p, qd[j], kd[j], vd[j], out=od[j])
+            else:
+                cache.append(p, kd[j], vd[j])
+                cache.decode(p, qd[j], out=od[j])
+            dec_done[j].record(comp)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(dec_done[j])
+                oh[p].copy_(od[j], non_blocking=True)
+                buf_free[j].record(d2h_s)
+
+    for _ in range(W):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    done = torch.cuda.Event()
+    if flush_buf is None:
+        a.record(comp)
+        for _ in range(K):
+            e2e_step()
+        done.record(d2h_s)                            # the last D2H copies are inside the timed region
+        comp.wait_event(done)
+        b.record(comp)
+        torch.cuda.synchronize()
+        e_local = a.elapsed_time(b)
+    else:
+        e_local = 0.0
+        for k in range(K):                            # flush, then one step with its copies
+            flush_buf.fill_(k & 0xff)
+            a.record(comp)
+            e2e_step()
+            done.record(d2h_s)
+            comp.wait_event(done)
+            b.record(comp)
+            torch.cuda.synchronize()
+            e_local += a.elapsed_time(b)
+    barrier()
+    e_ms = max_over_ranks(e_local)
+    h2d = L * B * (hq + 2 * hkv) * D * es * world
+    d2h = L * B * h_out * D * es * world
+    return {"value": total_tokens / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / K,
+            "bytes_counted": "whole job (sum over ranks)",
+            "path": "pinned host [q|k|v] -> one H2D copy per layer on an H2D stream (double-buffered, overlapped "
+                    "with the previous layer) -> PagedKVCache.append/decode (C ABI) "
+                    + ("-> head all-gather -> D2H of the gathered [Hq][B][D] " if head_mode else
+                       "-> D2H of out ") + "on a D2H stream -> pinned host"}
+
+
+def cost_model_check(w, wl, ctx_mean, measured_us, hq, hkv):
+    """a8 + f2 at the benched operating point: predict the layer-call time from the
+    committed calibrated table (profiles/cost_table_b200.json, built for full-head
+    LLaMA-3.1-8B GQA calls), then feed the measured time to apex_cost_observe and
+    predict again (online recalibration)."""
+    from paper_2506_03296_b200 import apex as A
+    with open(os.path.join(ROOT, "profiles", "cost_table_b200.json")) as f:
+        tab = json.load(f)
+    if (w.num_q_heads, w.num_kv_heads, w.dtype) != (32, 8, "bf16") or (hq, hkv) != (32, 8):
+        return {"skipped": "the calibrated table covers full-head LLaMA-3.1-8B GQA bf16 calls only"}
+    batch, kv_tokens = len(wl["ctx"]), int(round(ctx_mean * len(wl["ctx"])))
+    h = A.apex_cost_create(tab["batch"], tab["kv_tokens"], tab["us"])
+    try:
+        pred = A.apex_predict_time(h, batch, kv_tokens)
+        out = {"batch": batch, "kv_tokens": kv_tokens, "predicted_us": pred, "measured_us": measured_us,
+               "rel_err": (pred - measured_us) / measured_us}
+        if hasattr(A, "apex_cost_observe"):
+            A.apex_cost_observe(h, batch, kv_tokens, measured_us, 0.5)
+            out["predicted_us_after_observe"] = A.apex_predict_time(h, batch, kv_tokens)
+        return out
+    finally:
+        A.apex_cost_destroy(h)
 
 
 def _cpu_model():
@@ -635,8 +790,40 @@ def _cpu_model():
         return None
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args):
+    """--gpus N without WORLD_SIZE: re-run this script under torch.distributed.run with N
+    ranks (one per GPU; if fewer GPUs are visible, N ranks share GPU 0 over gloo)."""
+    n_dev = 0
+    try:
+        import torch
+        n_dev = torch.cuda.device_count()
+    except Exception:
+        pass
+    env = dict(os.environ)
+    argv = list(sys.argv[1:])
+    if args.impl == "apex" and n_dev < args.gpus:
+        env["APEX_BENCH_SAME_DEVICE"] = "1"
+        if "--dist-backend" not in argv:
+            argv += ["--dist-backend", "gloo"]
+        sys.stderr.write(f"bench.py: {n_dev} GPU(s) visible for --gpus {args.gpus}: ranks share GPU 0 over gloo "
+                         "(logic check, throughput not meaningful)\n")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

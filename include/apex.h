@@ -144,17 +144,44 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
 apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, void *out,
                                   float scale, apex_stream stream);
 
-/* As apex_decode_attention, but every output row is written to each of the
-   n_out (1..8) destinations outs[i] at element offset
-   b*out_row_stride + (out_head_offset + h)*D, h = this handle's q head.
-   With head sharding, rank r passes the symmetric (peer-mapped, e.g. over
-   NVLink) output buffers of all ranks and out_head_offset = r*Hq_local, so the
-   all-gather of head-sharded outputs happens inside the epilogue (SURVEY.md
-   §8(f) f3).  out_row_stride is in elements, a multiple of 4 and
-   >= (out_head_offset + Hq)*D; destinations 16-byte aligned. */
+/* As apex_decode_attention, but the output D-vector of (batch row b, local q head
+   h) is written to each of the n_out (1..8) destinations outs[i] at element offset
+       b*out_row_stride + (out_head_offset + h)*out_head_stride
+   (row-major [B][H][D]: row stride H*D, head stride D; head-major [H][B][D]: row
+   stride D, head stride B*D).  Strides are in elements, multiples of 4, and rows /
+   heads must not overlap (out_head_stride >= D and out_row_stride >= (offset+Hq) *
+   head stride, or out_row_stride >= D and out_head_stride >= B * row stride);
+   destinations 16-byte aligned.  Head sharding: rank r writes
+   its head slice head-major into a local [Hq/N][B][D] buffer that NCCL all-gathers
+   into [Hq][B][D] with no permute; or (f3) it passes the symmetric, peer-mapped
+   [Hq][B][D] buffers of all ranks with out_head_offset = r*Hq/N, so the all-gather
+   happens inside the epilogue.
+   signals: NULL, or n_out device pointers (peer-mapped allowed) to uint32 arrays;
+   after every output row of this call is stored in every destination, the call's
+   last launch writes signals[i][signal_slot] = signal_value with a system-scope
+   release (one in-kernel completion flag per layer-call, no host barrier).  A
+   reader waits with apex_signal_wait before it reads the rows.  Other errors as
+   apex_decode_attention; APEX_EINVAL on overlapping strides or bad signals. */
 apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
-                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
-                                     apex_stream stream);
+                                     int64_t out_row_stride, int64_t out_head_stride, int32_t out_head_offset,
+                                     uint32_t *const *signals, int32_t signal_slot, uint32_t signal_value,
+                                     float scale, apex_stream stream);
+
+/* Enqueue on `stream` a one-warp kernel that waits until every signals[i] (device
+   uint32, i < n) has reached `value` (wrap-safe: (int32_t)(signals[i] - value) >= 0)
+   with system-scope acquire loads, so later work on the stream sees the rows the
+   signalling launches stored (f3 completion flag; PAPER.md P:82 analogue).  If
+   timeout_ns elapses first the kernel stops waiting and, if status != NULL,
+   writes 1 to the device word *status (callers check it; nothing hangs).
+   APEX_EINVAL on NULL/misaligned pointers or n < 1. */
+apex_status apex_signal_wait(const uint32_t *signals, int32_t n, uint32_t value, uint64_t timeout_ns,
+                             uint32_t *status, apex_stream stream);
+
+/* Enqueue a kernel that writes `value` into dst[i][slot] (i < n_dst <= 8, device or
+   peer-mapped uint32 arrays) with a system-scope release, after everything earlier
+   on `stream`.  Used by a reader to hand a consumed symmetric buffer back to the
+   writers (write-after-read guard of the fused gather). */
+apex_status apex_signal_post(uint32_t *const *dst, int32_t n_dst, int32_t slot, uint32_t value, apex_stream stream);
 
 /* apex_kv_append + apex_decode_attention in ONE launch for
    a pure decode step: every sequence of the last apex_kv_alloc has exactly one
@@ -231,6 +258,25 @@ apex_status apex_cost_create(const int32_t *batch, int32_t nb, const int64_t *kv
    the grid's edges on each axis (reading c16).  Pure host computation. */
 apex_status apex_predict_time(const apex_cost *cost, int32_t batch, int64_t kv_tokens,
                               double *us_out);
+/* Online recalibration from one measured per-layer-call time (§6:
+   online profiling to correct the offline profile's mispredictions; the update
+   rule is DESIGN.md reading c17):
+     1. if (batch, kv_tokens) lies outside the grid on an axis, a grid line through
+        it is added on that axis, valued at the current (clamped) predictions --
+        no prediction changes;
+     2. with e = measured_us - predicted and w_c the bilinear weights of the four
+        corners of the point's cell, corner c += alpha * e * w_c / sum_c w_c^2
+        (normalised LMS): the prediction at the point becomes exactly
+        predicted + alpha * e; predictions whose cell shares no corner with
+        it are unchanged.
+   alpha in (0, 1] (1: trust the measurement fully; smaller: EWMA-like smoothing),
+   measured_us finite and > 0, at most 256 grid points per axis; otherwise
+   APEX_EINVAL and the table is unchanged.  Pure host computation. */
+apex_status apex_cost_observe(apex_cost *cost, int32_t batch, int64_t kv_tokens, double measured_us,
+                              double alpha);
+/* Current grid sizes, and a copy of the grid and times (arrays of nb, nk, nb*nk). */
+apex_status apex_cost_size(const apex_cost *cost, int32_t *nb, int32_t *nk);
+apex_status apex_cost_table(const apex_cost *cost, int32_t *batch, int64_t *kv_tokens, double *us);
 void apex_cost_destroy(apex_cost *cost);
 
 /* ---- APEX decision layer (§3.2 Eq1-Eq6, Algorithm 1) ---- */

@@ -8,6 +8,15 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import 
   performance model); the interpolation scheme is unstated, so we take SPEC.md
   S:49-57 / S:91's reading (reading c16): bilinear over the
   (batch, kv_tokens) grid, clamped to the grid's edges on each axis.
+* ``observe`` — online recalibration of that table from a measured time,
+  PAPER.md P:503 (§6: "online profiling specifically for decode-intensive
+  scenarios" to correct mispredictions of the offline profile).  The paper gives
+  no update rule; reading c17 fixes one: (1) a point outside the grid
+  first adds a grid line through it, valued at the current (clamped) predictions,
+  so no prediction changes; (2) the four corners of the point's cell move by a
+  normalised least-mean-squares step, corner c += alpha * e * w_c / sum(w^2) with
+  e = measured - predicted and w_c the bilinear weights, after which the
+  prediction at the point is exactly predicted + alpha * e.
 * Eq1-Eq6 of §3.2 written out as printed.
 """
 from __future__ import annotations
@@ -33,6 +42,40 @@ def interp(batch_grid, kv_grid, us, batch, kv_tokens) -> float:
     j1 = min(j + 1, len(kv_grid) - 1)
     return ((1 - fx) * (1 - fy) * us[i][j] + fx * (1 - fy) * us[i1][j]
             + (1 - fx) * fy * us[i][j1] + fx * fy * us[i1][j1])
+
+
+def observe(batch_grid, kv_grid, us, batch, kv_tokens, measured_us, alpha):
+    """One online-recalibration step (reading c17).  Returns new (batch_grid, kv_grid, us);
+    the inputs are not modified."""
+    if not (0.0 < alpha <= 1.0) or not (measured_us > 0.0) or measured_us == float("inf"):
+        raise ValueError("alpha must be in (0, 1] and measured_us finite and > 0")
+    bg, kg = list(batch_grid), list(kv_grid)
+    u = [list(row) for row in us]
+    # (1) grid lines through an outside point, valued at the current predictions
+    if batch < bg[0] or batch > bg[-1]:
+        row = [interp(bg, kg, u, batch, k) for k in kg]
+        at = 0 if batch < bg[0] else len(bg)
+        bg.insert(at, batch)
+        u.insert(at, row)
+    if kv_tokens < kg[0] or kv_tokens > kg[-1]:
+        col = [interp(bg, kg, u, b, kv_tokens) for b in bg]
+        at = 0 if kv_tokens < kg[0] else len(kg)
+        kg.insert(at, kv_tokens)
+        for i in range(len(bg)):
+            u[i].insert(at, col[i])
+    # (2) normalised LMS step on the corners of the point's cell
+    e = measured_us - interp(bg, kg, u, batch, kv_tokens)
+    i, fx = _axis(bg, batch)
+    j, fy = _axis(kg, kv_tokens)
+    i1, j1 = min(i + 1, len(bg) - 1), min(j + 1, len(kg) - 1)
+    w = {}
+    for (a, b), wt in (((i, j), (1 - fx) * (1 - fy)), ((i1, j), fx * (1 - fy)),
+                       ((i, j1), (1 - fx) * fy), ((i1, j1), fx * fy)):
+        w[(a, b)] = w.get((a, b), 0.0) + wt
+    norm = sum(x * x for x in w.values())
+    for (a, b), wt in w.items():
+        u[a][b] += alpha * e * wt / norm
+    return bg, kg, u
 
 
 def t_gpuonly(t_glinear, t_gatt):            # Eq1, P:172-174

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint32, c_uint64, c_void_p
 
 LIB_PATH = os.environ.get("APEX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libapex.so")
 
@@ -26,7 +26,8 @@ EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex
            "apex_kv_num_free_blocks", "apex_kv_seq_info", "apex_kv_last_slots", "apex_kv_plan", "apex_kv_plan_ranges",
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
            "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex",
-           "apex_decode_attention_append"]
+           "apex_decode_attention_append", "apex_signal_wait", "apex_signal_post", "apex_cost_observe",
+           "apex_cost_size", "apex_cost_table"]
 STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
 
 
@@ -96,7 +97,13 @@ def lib():
             "apex_decide": (c_int, [POINTER(apex_sched_input), POINTER(apex_decision)]),
             "apex_kv_decode_launches": (c_int32, [c_void_p]),
             "apex_decode_attention_ex": (c_int, [c_void_p, c_int32, c_void_p, POINTER(c_void_p), c_int32, c_int64,
-                                                 c_int32, c_float, c_void_p]),
+                                                 c_int64, c_int32, POINTER(c_void_p), c_int32, c_uint32, c_float,
+                                                 c_void_p]),
+            "apex_cost_observe": (c_int, [c_void_p, c_int32, c_int64, c_double, c_double]),
+            "apex_cost_size": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32)]),
+            "apex_cost_table": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+            "apex_signal_wait": (c_int, [c_void_p, c_int32, c_uint32, c_uint64, c_void_p, c_void_p]),
+            "apex_signal_post": (c_int, [POINTER(c_void_p), c_int32, c_int32, c_uint32, c_void_p]),
             "apex_decode_attention_append": (c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                                      c_float, c_void_p]),
         }
@@ -227,6 +234,19 @@ def apex_predict_time(cost: int, batch: int, kv_tokens: int) -> float:
     return out.value
 
 
+def apex_cost_observe(cost: int, batch: int, kv_tokens: int, measured_us: float, alpha: float = 1.0) -> None:
+    _check(lib().apex_cost_observe(cost, int(batch), int(kv_tokens), float(measured_us), float(alpha)))
+
+
+def apex_cost_table(cost: int):
+    """(batch_grid, kv_grid, us[nb][nk]) of the current table."""
+    nb, nk = c_int32(), c_int32()
+    _check(lib().apex_cost_size(cost, ctypes.byref(nb), ctypes.byref(nk)))
+    bg, kg, us = (c_int32 * nb.value)(), (c_int64 * nk.value)(), (c_double * (nb.value * nk.value))()
+    _check(lib().apex_cost_table(cost, bg, kg, us))
+    return list(bg), list(kg), [list(us[i * nk.value:(i + 1) * nk.value]) for i in range(nb.value)]
+
+
 def apex_cost_destroy(cost: int) -> None:
     lib().apex_cost_destroy(cost)
 
@@ -241,8 +261,7 @@ def apex_synth_rows(out_ptr: int, dtype: str, tensor: int, layer: int, row_b_ptr
 def apex_pipelining_threshold(t_glinear: float, t_gatt: float) -> float:
     out = c_double()
     st = lib().apex_pipelining_threshold(float(t_glinear), float(t_gatt), ctypes.byref(out))
-    if st != APEX_OK:
-        raise ApexError(st, "apex_pipelining_threshold: times must be finite and > 0")
+    _check(st)
     return out.value
 
 
@@ -253,8 +272,7 @@ def apex_decide(n_prefill: int, n_gpu_decode: int, n_cpu_decode: int, n_g: float
                            t_gatt_pref, min_cpu_ratio)
     out = apex_decision()
     st = lib().apex_decide(ctypes.byref(inp), ctypes.byref(out))
-    if st != APEX_OK:
-        raise ApexError(st, "apex_decide: invalid input")
+    _check(st)
     return {"strategy": STRATEGIES[out.strategy], "gate_closed": bool(out.gate_closed), "lhs": out.lhs,
             "rhs": out.rhs, "eq6_threshold": out.eq6_threshold}
 
@@ -263,8 +281,26 @@ def apex_kv_decode_launches(kv: int) -> int:
     return int(lib().apex_kv_decode_launches(kv))
 
 
-def apex_decode_attention_ex(kv: int, layer: int, q_ptr: int, out_ptrs, out_row_stride: int, out_head_offset: int,
-                             scale: float, stream: int = 0) -> None:
+def apex_decode_attention_ex(kv: int, layer: int, q_ptr: int, out_ptrs, out_row_stride: int, out_head_stride: int,
+                             out_head_offset: int, scale: float, stream: int = 0, signal_ptrs=None,
+                             signal_slot: int = 0, signal_value: int = 0) -> None:
     outs = (c_void_p * max(len(out_ptrs), 1))(*[int(x) for x in out_ptrs])
+    sig = None
+    if signal_ptrs is not None:
+        if len(signal_ptrs) != len(out_ptrs):
+            raise ValueError("one signal array per destination")
+        sig = (c_void_p * len(signal_ptrs))(*[int(x) for x in signal_ptrs])
     _check(lib().apex_decode_attention_ex(kv, int(layer), q_ptr, outs, len(out_ptrs), int(out_row_stride),
-                                          int(out_head_offset), float(scale), stream))
+                                          int(out_head_stride), int(out_head_offset), sig, int(signal_slot),
+                                          int(signal_value) & 0xffffffff, float(scale), stream))
+
+
+def apex_signal_wait(signals_ptr: int, n: int, value: int, timeout_ns: int, status_ptr: int = 0,
+                     stream: int = 0) -> None:
+    _check(lib().apex_signal_wait(signals_ptr, int(n), int(value) & 0xffffffff, int(timeout_ns), status_ptr or None,
+                                  stream))
+
+
+def apex_signal_post(dst_ptrs, slot: int, value: int, stream: int = 0) -> None:
+    dst = (c_void_p * max(len(dst_ptrs), 1))(*[int(x) for x in dst_ptrs])
+    _check(lib().apex_signal_post(dst, len(dst_ptrs), int(slot), int(value) & 0xffffffff, stream))

@@ -26,16 +26,34 @@ using apex::MergeItem;
 using apex::WorkItem;
 
 namespace {
+apex_status vfail(apex_status st, const char *fmt, va_list ap);
+}
+
+// thread-local error text for the other translation units (sched.cpp)
+apex_status apex::set_error(apex_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vfail(st, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+namespace {
 
 thread_local std::string g_err;
 
-apex_status fail(apex_status st, const char *fmt, ...) {
+apex_status vfail(apex_status st, const char *fmt, va_list ap) {
     char buf[512];
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    g_err = buf;
+    return st;
+}
+
+apex_status fail(apex_status st, const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
+    vfail(st, fmt, ap);
     va_end(ap);
-    g_err = buf;
     return st;
 }
 
@@ -91,8 +109,8 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     up += align_up(sizeof(int32_t) * (size_t)d->max_new_tokens, 256);
     up += align_up(sizeof(int2) * (size_t)w.max_bt_delta, 256);
     up += align_up(sizeof(int2) * (size_t)d->max_batch, 256);
-    w.counters = 0;                                           // 2 counters x 64 layers
-    w.merge_counters = 512;                                   // one per split pair
+    w.counters = 0;                                           // 3 counters x 64 layers (queue, done, signal)
+    w.merge_counters = 1024;                                  // one per split pair
     w.upload = align_up(w.merge_counters + sizeof(int32_t) * (size_t)w.max_merges, 256);
     w.upload_cap = up;
     w.part_o = align_up(w.upload + up, 256);
@@ -198,7 +216,7 @@ struct apex_kv {
     int32_t forced_chunk_blocks = 0;
     int32_t grid_override = 0;
     int32_t dyn_permille = kDefaultDynPermille;   // apex_kv_set_sched
-    int64_t latency_tiles_per_cta = 512;          // latency regime while T <= this * P (APEX_LAT_TILES: tuning)
+    int64_t latency_tiles_per_cta = 512;          // latency regime while T <= this * P
     int32_t guided[4] = {8, 900, 950, 980};       // guided: T/(g0 P) chunk, halved from permille g1, g2, g3
     int32_t plan_grid = 0;                        // CTAs the last plan was made for (= launch grid)
     std::vector<int32_t> cta_begin;               // [plan_grid + 1]
@@ -253,7 +271,6 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
     kv->sm_count = query_sm_count(kv->host_only);
     kv->ws = layout_for(desc, kv->sm_count);
     kv->seqs.resize(desc->max_seqs);
-    if (const char *e = std::getenv("APEX_LAT_TILES")) kv->latency_tiles_per_cta = std::max(1, std::atoi(e));
     kv->free_stack.resize(desc->num_blocks);
     for (int32_t i = 0; i < desc->num_blocks; ++i) kv->free_stack[i] = desc->num_blocks - 1 - i;
     if (!kv->host_only) {
@@ -300,6 +317,9 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
         }
         // zero the work-queue and merge counters once; kernels leave them at zero
         e = cudaMemset((uint8_t *)desc->workspace + kv->ws.counters, 0, kv->ws.upload);
+        // create is not on the hot path: finish the memset before any launch on any stream
+        // (a caller's non-blocking stream is not ordered after the legacy default stream)
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             apex_kv_destroy(kv);
             return cuda_fail(e, "apex_kv_create: counters");
@@ -460,7 +480,20 @@ static void plan_streamk(const std::vector<int32_t> &nblks, int32_t Hkv, int64_t
         }
 }
 
-static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
+namespace {
+// Result of planning one step; committed into the handle only when the whole
+// apex_kv_alloc call succeeds (all-or-nothing, include/apex.h).
+struct Plan {
+    std::vector<WorkItem> items;
+    std::vector<MergeItem> merges;
+    std::vector<int32_t> cta_begin;
+    bool fuse_merge = false;
+    int32_t grid = 0;
+};
+}  // namespace
+
+static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_of_row,
+                             const std::vector<int32_t> &lens, Plan &out) {
     const int32_t Hkv = kv->d.num_kv_heads, B = (int32_t)lens.size();
     const int64_t P = std::max<int64_t>(1, kv->grid_override > 0
                                                ? kv->grid_override
@@ -526,8 +559,6 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
         // tiles (flattened order) are cut into halved, quartered, ... chunks, so the
         // queue (longest first) ends with small items and the CTAs finish together
         const bool guided = !latency && kv->forced_chunk_blocks == 0 && kv->dyn_permille == -2;
-        if (const char *e = guided ? std::getenv("APEX_GUIDED") : nullptr)   // tuning aid: "div,pm1,pm2,pm3"
-            std::sscanf(e, "%d,%d,%d,%d", &kv->guided[0], &kv->guided[1], &kv->guided[2], &kv->guided[3]);
         if (guided) chunk = std::max<int64_t>(16, cdiv(T, (int64_t)kv->guided[0] * P));
         int64_t pos = 0;
         for (int32_t b = 0; b < B; ++b) {
@@ -559,7 +590,7 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
             const int32_t mg = split ? (int32_t)merges.size() : -1;
             if (split) merges.push_back({b, g, parts, (int32_t)pp.size()});
             for (size_t i = 0; i < pp.size(); ++i) {
-                const WorkItem w{b, g, pp[i].blk0, pp[i].nblk, split ? parts + (int32_t)i : -1, kv->batch_seq[b],
+                const WorkItem w{b, g, pp[i].blk0, pp[i].nblk, split ? parts + (int32_t)i : -1, seq_of_row[b],
                                  lens[b], mg};
                 (pp[i].cta >= 0 ? st_items[pp[i].cta] : dyn).push_back(w);
             }
@@ -570,24 +601,24 @@ static apex_status plan_step(apex_kv *kv, const std::vector<int32_t> &lens) {
         return fail(APEX_EINVAL, "split chunk of %lld tokens yields %zu work items > workspace capacity %d",
                     (long long)chunk * kv->d.block_size, n_items, kv->ws.max_items);
     std::stable_sort(dyn.begin(), dyn.end(), [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
-    std::vector<WorkItem> items;
+    std::vector<WorkItem> &items = out.items;
+    items.clear();
     items.reserve(n_items);
-    kv->cta_begin.assign((size_t)P + 1, 0);
+    out.cta_begin.assign((size_t)P + 1, 0);
     if (streamk) {
         for (int64_t c = 0; c < P; ++c) {
-            kv->cta_begin[c] = (int32_t)items.size();
+            out.cta_begin[c] = (int32_t)items.size();
             items.insert(items.end(), st_items[c].begin(), st_items[c].end());
         }
-        kv->cta_begin[P] = (int32_t)items.size();
+        out.cta_begin[P] = (int32_t)items.size();
     } else {
         // CTA c starts with item c (no queue round trip on the launch path), then the queue
-        for (int64_t c = 0; c <= P; ++c) kv->cta_begin[c] = (int32_t)std::min<int64_t>(c, (int64_t)dyn.size());
+        for (int64_t c = 0; c <= P; ++c) out.cta_begin[c] = (int32_t)std::min<int64_t>(c, (int64_t)dyn.size());
     }
     items.insert(items.end(), dyn.begin(), dyn.end());
-    kv->items.swap(items);
-    kv->merges.swap(merges);
-    kv->fuse_merge = latency;
-    kv->plan_grid = (int32_t)P;
+    out.merges.swap(merges);
+    out.fuse_merge = latency;
+    out.grid = (int32_t)P;
     return APEX_OK;
 }
 
@@ -596,8 +627,10 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     if (!seq_ids || !n_new || n < 1 || n > kv->d.max_batch)
         return fail(APEX_EINVAL, "batch of %d sequences not in [1, max_batch=%d]", n, kv->d.max_batch);
     const int32_t bs = kv->d.block_size;
-    // ---- validate everything before touching any state (all-or-nothing)
+    // ---- 1. validate, plan and size the upload on the would-be lengths, before touching
+    // any state: every failure below leaves the handle exactly as it was (all-or-nothing)
     std::vector<char> seen(kv->d.max_seqs, 0);
+    std::vector<int32_t> lens(n);
     int64_t need = 0, rows = 0;
     for (int32_t i = 0; i < n; ++i) {
         const int32_t s = seq_ids[i], k = n_new[i];
@@ -611,20 +644,45 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
             return fail(APEX_EINVAL, "seq %d would exceed max context %d", s, kv->d.max_blocks_per_seq * bs);
         need += cdiv(L + k, bs) - cdiv(L, bs);
         rows += k;
+        lens[i] = (int32_t)(L + k);
     }
     if (rows > kv->d.max_new_tokens)
         return fail(APEX_EINVAL, "%lld new tokens > max_new_tokens %d", (long long)rows, kv->d.max_new_tokens);
     if (need > (int64_t)kv->free_stack.size())
         return fail(APEX_ENOBLOCKS, "need %lld blocks, %zu free", (long long)need, kv->free_stack.size());
+    std::vector<int32_t> seq_of_row(seq_ids, seq_ids + n);
+    Plan plan;
+    apex_status st = plan_step(kv, seq_of_row, lens, plan);
+    if (st != APEX_OK) return st;
+    // packed upload: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
+    // len deltas -- one H2D copy of exactly the used bytes; kernels find the merge list and
+    // the slot map through offsets in the header (fixed launch parameters)
+    const size_t items_bytes = sizeof(WorkItem) * plan.items.size();
+    const size_t merges_bytes = sizeof(MergeItem) * plan.merges.size();
+    const size_t o_merges = align_up(kv->ws.o_items + items_bytes, 256);
+    const size_t o_slots = o_merges + align_up(merges_bytes, 256);
+    const size_t o_bt = o_slots + align_up(sizeof(int32_t) * (size_t)rows, 256);
+    const size_t o_len = o_bt + align_up(sizeof(int2) * (size_t)need, 256);
+    const size_t up_end = o_len + align_up(sizeof(int2) * (size_t)n, 256);
+    if (!kv->host_only && up_end > kv->ws.upload_cap)
+        return fail(APEX_EINVAL, "step metadata (%zu B) exceeds the upload region (%zu B)", up_end, kv->ws.upload_cap);
+    const int r = kv->ring;
+    if (!kv->host_only && kv->staged_pending[r]) {
+        cudaError_t e = cudaEventSynchronize(kv->staged[r]);   // its previous H2D must be done
+        if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: staging reuse");
+        kv->staged_pending[r] = false;
+    }
 
-    // ---- commit: pop blocks, compute slots and deltas
+    // ---- 2. commit: pop blocks, compute slots and deltas (cannot fail)
     std::vector<int32_t> slots;
     slots.reserve(rows);
     std::vector<int2> bt_delta, len_delta;
-    std::vector<int32_t> lens(n);
-    kv->batch_seq.assign(seq_ids, seq_ids + n);
+    std::vector<int32_t> popped;                       // pop order (for the CUDA-failure rollback)
+    std::vector<apex_kv::Seq> before(n);               // (live, len) of each seq before the call
     for (int32_t i = 0; i < n; ++i) {
         auto &sq = kv->seqs[seq_ids[i]];
+        before[i].live = sq.live;
+        before[i].len = sq.len;
         if (!sq.live) {
             sq.live = true;
             sq.len = 0;
@@ -634,72 +692,72 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
             if (pos % bs == 0) {
                 const int32_t blk = kv->free_stack.back();
                 kv->free_stack.pop_back();
+                popped.push_back(blk);
                 bt_delta.push_back({seq_ids[i] * kv->d.max_blocks_per_seq + pos / bs, blk});
                 sq.blocks.push_back(blk);
             }
             slots.push_back(sq.blocks[pos / bs] * bs + pos % bs);
         }
         sq.len += n_new[i];
-        lens[i] = sq.len;
         len_delta.push_back({seq_ids[i], sq.len});
     }
+    auto rollback = [&] {
+        for (int32_t i = n - 1; i >= 0; --i) {
+            auto &sq = kv->seqs[seq_ids[i]];
+            const size_t nb = (size_t)cdiv(before[i].len, bs);
+            sq.blocks.resize(before[i].live ? nb : 0);
+            sq.len = before[i].len;
+            sq.live = before[i].live;
+        }
+        for (auto it = popped.rbegin(); it != popped.rend(); ++it) kv->free_stack.push_back(*it);
+    };
+    if (!kv->host_only) {
+        // ---- 3. pack the step metadata into pinned staging and upload it
+        uint8_t *host = kv->staging[r];
+        apex::StepHeader hdr{};
+        hdr.n_items = (int32_t)plan.items.size();
+        hdr.n_merges = (int32_t)plan.merges.size();
+        hdr.n_rows = (int32_t)rows;
+        hdr.o_merges = (int32_t)o_merges;
+        hdr.o_slots = (int32_t)o_slots;
+        std::memcpy(host, &hdr, sizeof hdr);
+        std::memcpy(host + apex::kCtaBeginOffset, plan.cta_begin.data(), sizeof(int32_t) * plan.cta_begin.size());
+        if (items_bytes) std::memcpy(host + kv->ws.o_items, plan.items.data(), items_bytes);
+        if (merges_bytes) std::memcpy(host + o_merges, plan.merges.data(), merges_bytes);
+        if (rows) std::memcpy(host + o_slots, slots.data(), sizeof(int32_t) * slots.size());
+        if (need) std::memcpy(host + o_bt, bt_delta.data(), sizeof(int2) * bt_delta.size());
+        std::memcpy(host + o_len, len_delta.data(), sizeof(int2) * len_delta.size());
+        uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaError_t e = cudaMemcpyAsync(dev, host, up_end, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
+        if (e == cudaSuccess) {
+            kv->staged_pending[r] = true;
+            e = apex::launch_apply_deltas((const int2 *)(dev + o_bt), (int)bt_delta.size(),
+                                          (const int2 *)(dev + o_len), (int)len_delta.size(), kv->d.block_table,
+                                          kv->d.seq_lens, s);
+        }
+        if (e != cudaSuccess) {
+            rollback();
+            // the device header may already hold the withdrawn step: append/decode are
+            // refused until the next successful alloc
+            kv->have_step = false;
+            return cuda_fail(e, "apex_kv_alloc: metadata upload");
+        }
+        kv->ring ^= 1;
+    }
+    kv->batch_seq.swap(seq_of_row);
     kv->slots.swap(slots);
+    kv->items.swap(plan.items);
+    kv->merges.swap(plan.merges);
+    kv->cta_begin.swap(plan.cta_begin);
+    kv->fuse_merge = plan.fuse_merge;
+    kv->plan_grid = plan.grid;
     kv->batch = n;
     kv->n_rows = (int32_t)rows;
     kv->have_step = true;
     kv->single_token_step = true;
     for (int32_t i = 0; i < n; ++i) kv->single_token_step = kv->single_token_step && n_new[i] == 1;
-    apex_status st = plan_step(kv, lens);
-    if (st != APEX_OK) {
-        kv->have_step = false;   // blocks stay allocated (state is consistent); the step is unusable
-        return st;
-    }
-    if (kv->host_only) return APEX_OK;
-
-    // ---- pack the step metadata into pinned staging and upload it
-    const int r = kv->ring;
-    kv->ring ^= 1;
-    if (kv->staged_pending[r]) {
-        cudaError_t e = cudaEventSynchronize(kv->staged[r]);   // its previous H2D must be done
-        if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: staging reuse");
-        kv->staged_pending[r] = false;
-    }
-    uint8_t *host = kv->staging[r];
-    // packed: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
-    // len deltas -- one H2D copy of exactly the used bytes; kernels find the merge
-    // list and the slot map through offsets in the header (fixed launch parameters)
-    const size_t items_bytes = sizeof(WorkItem) * kv->items.size();
-    const size_t merges_bytes = sizeof(MergeItem) * kv->merges.size();
-    std::memcpy(host + apex::kCtaBeginOffset, kv->cta_begin.data(), sizeof(int32_t) * kv->cta_begin.size());
-    std::memcpy(host + kv->ws.o_items, kv->items.data(), items_bytes);
-    size_t off = align_up(kv->ws.o_items + items_bytes, 256);
-    auto put = [&](const void *src, size_t bytes) {
-        const size_t at = off;
-        if (bytes) std::memcpy(host + at, src, bytes);
-        off = align_up(off + bytes, 256);
-        return at;
-    };
-    const size_t o_merges = put(kv->merges.data(), merges_bytes);
-    const size_t o_slots = put(kv->slots.data(), sizeof(int32_t) * kv->slots.size());
-    const size_t o_bt = put(bt_delta.data(), sizeof(int2) * bt_delta.size());
-    const size_t o_len = put(len_delta.data(), sizeof(int2) * len_delta.size());
-    if (off > kv->ws.upload_cap) return fail(APEX_EINVAL, "step metadata exceeds the upload region");
-    apex::StepHeader hdr{};
-    hdr.n_items = (int32_t)kv->items.size();
-    hdr.n_merges = (int32_t)kv->merges.size();
-    hdr.n_rows = (int32_t)rows;
-    hdr.o_merges = (int32_t)o_merges;
-    hdr.o_slots = (int32_t)o_slots;
-    std::memcpy(host, &hdr, sizeof hdr);
-    uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
-    cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
-    if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: metadata upload");
-    kv->staged_pending[r] = true;
-    e = apex::launch_apply_deltas((const int2 *)(dev + o_bt), (int)bt_delta.size(), (const int2 *)(dev + o_len),
-                                  (int)len_delta.size(), kv->d.block_table, kv->d.seq_lens, s);
-    if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: apply deltas");
     return APEX_OK;
 }
 
@@ -732,25 +790,40 @@ apex_status apex_decode_attention(apex_kv *kv, int32_t layer, const void *q, voi
                                   apex_stream stream) {
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");
     void *outs[1] = {out};
-    return apex_decode_attention_ex(kv, layer, q, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim, 0, scale,
-                                    stream);
+    return apex_decode_attention_ex(kv, layer, q, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim,
+                                    kv->d.head_dim, 0, nullptr, 0, 0, scale, stream);
 }
 
 }  // extern "C"
 
 static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const void *k_new, const void *v_new,
-                               void *const *outs, int32_t n_out, int64_t out_row_stride, int32_t out_head_offset,
-                               float scale, apex_stream stream) {
+                               void *const *outs, int32_t n_out, int64_t out_row_stride, int64_t out_head_stride,
+                               int32_t out_head_offset, uint32_t *const *signals, int32_t signal_slot,
+                               uint32_t signal_value, float scale, apex_stream stream) {
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");
     if (kv->host_only) return fail(APEX_EINVAL, "host-only handle has no device pools");
     if (!kv->have_step) return fail(APEX_EINVAL, "apex_decode_attention before apex_kv_alloc");
     if (layer < 0 || layer >= kv->d.num_layers) return fail(APEX_EINVAL, "layer %d out of range", layer);
     if (!q || !outs || n_out < 1 || n_out > apex::kMaxOut)
         return fail(APEX_EINVAL, "q/outs is NULL or n_out %d not in [1, %d]", n_out, apex::kMaxOut);
-    if (out_head_offset < 0 || out_row_stride % 4 ||
-        out_row_stride < (int64_t)(out_head_offset + kv->d.num_q_heads) * kv->d.head_dim)
-        return fail(APEX_EINVAL, "out_row_stride %lld / out_head_offset %d do not fit %d heads",
-                    (long long)out_row_stride, out_head_offset, kv->d.num_q_heads);
+    // every (row, head) of the step owns a disjoint D-vector of each destination:
+    // row-major-like (row stride covers all heads) or head-major-like (head stride
+    // covers all rows), strides multiples of 4 elements (8/16-byte vector stores)
+    const int64_t D = kv->d.head_dim, H = (int64_t)out_head_offset + kv->d.num_q_heads, B = kv->batch;
+    const bool row_major = out_head_stride >= D && out_row_stride >= H * out_head_stride;
+    const bool head_major = out_row_stride >= D && out_head_stride >= B * out_row_stride;
+    if (out_head_offset < 0 || out_row_stride % 4 || out_head_stride % 4 || !(row_major || head_major))
+        return fail(APEX_EINVAL,
+                    "out strides (row %lld, head %lld) / head offset %d: rows and heads of the %lld x %lld "
+                    "destination must not overlap",
+                    (long long)out_row_stride, (long long)out_head_stride, out_head_offset, (long long)B,
+                    (long long)H);
+    if (signals) {
+        if (signal_slot < 0) return fail(APEX_EINVAL, "signal_slot %d < 0", signal_slot);
+        for (int32_t i = 0; i < n_out; ++i)
+            if (!signals[i] || ((uintptr_t)signals[i] & 3))
+                return fail(APEX_EINVAL, "signals[%d] NULL or not 4-byte aligned", i);
+    }
     if ((uintptr_t)q & 15) return fail(APEX_EINVAL, "q not 16-byte aligned");
     for (int32_t i = 0; i < n_out; ++i)
         if (!outs[i] || ((uintptr_t)outs[i] & 15)) return fail(APEX_EINVAL, "outs[%d] NULL or not 16-byte aligned", i);
@@ -760,7 +833,12 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
     for (int32_t i = 0; i < n_out; ++i) p.out[i] = outs[i];
     p.n_out = n_out;
     p.out_row_stride = out_row_stride;
+    p.out_head_stride = out_head_stride;
     p.out_head_offset = out_head_offset;
+    if (signals)
+        for (int32_t i = 0; i < n_out; ++i) p.signals[i] = signals[i];
+    p.signal_slot = signal_slot;
+    p.signal_value = signal_value;
     p.block_table = kv->d.block_table;
     uint8_t *ws = (uint8_t *)kv->d.workspace;
     uint8_t *up = ws + kv->ws.upload;
@@ -771,6 +849,7 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
     p.part_o = (float *)(ws + kv->ws.part_o);
     p.part_ml = (float *)(ws + kv->ws.part_ml);
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
+    p.sig_counter = (int32_t *)(ws + kv->ws.counters) + 2 * apex::kMaxLayers + layer;
     p.merge_counters = (int32_t *)(ws + kv->ws.merge_counters);
     p.merge_grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kv->ws.max_merges, 16LL * kv->sm_count));
     p.max_blocks_per_seq = kv->d.max_blocks_per_seq;
@@ -812,9 +891,11 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
 extern "C" {
 
 apex_status apex_decode_attention_ex(apex_kv *kv, int32_t layer, const void *q, void *const *outs, int32_t n_out,
-                                     int64_t out_row_stride, int32_t out_head_offset, float scale,
-                                     apex_stream stream) {
-    return decode_impl(kv, layer, q, nullptr, nullptr, outs, n_out, out_row_stride, out_head_offset, scale, stream);
+                                     int64_t out_row_stride, int64_t out_head_stride, int32_t out_head_offset,
+                                     uint32_t *const *signals, int32_t signal_slot, uint32_t signal_value,
+                                     float scale, apex_stream stream) {
+    return decode_impl(kv, layer, q, nullptr, nullptr, outs, n_out, out_row_stride, out_head_stride, out_head_offset,
+                       signals, signal_slot, signal_value, scale, stream);
 }
 
 apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void *q, const void *k_new,
@@ -822,8 +903,27 @@ apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void 
     if (!kv) return fail(APEX_EINVAL, "kv is NULL");
     if (!k_new || !v_new) return fail(APEX_EINVAL, "k_new/v_new is NULL");
     void *outs[1] = {out};
-    return decode_impl(kv, layer, q, k_new, v_new, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim, 0, scale,
-                       stream);
+    return decode_impl(kv, layer, q, k_new, v_new, outs, 1, (int64_t)kv->d.num_q_heads * kv->d.head_dim,
+                       kv->d.head_dim, 0, nullptr, 0, 0, scale, stream);
+}
+
+apex_status apex_signal_wait(const uint32_t *signals, int32_t n, uint32_t value, uint64_t timeout_ns,
+                             uint32_t *status, apex_stream stream) {
+    if (!signals || n < 1 || ((uintptr_t)signals & 3))
+        return fail(APEX_EINVAL, "apex_signal_wait: signals NULL/misaligned or n %d < 1", n);
+    if (status && ((uintptr_t)status & 3)) return fail(APEX_EINVAL, "apex_signal_wait: status misaligned");
+    cudaError_t e = apex::launch_signal_wait(signals, n, value, timeout_ns, status, (cudaStream_t)stream);
+    return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_signal_wait");
+}
+
+apex_status apex_signal_post(uint32_t *const *dst, int32_t n_dst, int32_t slot, uint32_t value, apex_stream stream) {
+    if (!dst || n_dst < 1 || n_dst > apex::kMaxOut || slot < 0)
+        return fail(APEX_EINVAL, "apex_signal_post: dst NULL, n_dst %d not in [1, %d] or slot %d < 0", n_dst,
+                    apex::kMaxOut, slot);
+    for (int32_t i = 0; i < n_dst; ++i)
+        if (!dst[i] || ((uintptr_t)dst[i] & 3)) return fail(APEX_EINVAL, "apex_signal_post: dst[%d] NULL/misaligned", i);
+    cudaError_t e = apex::launch_signal_post(dst, n_dst, slot, value, (cudaStream_t)stream);
+    return e == cudaSuccess ? APEX_OK : cuda_fail(e, "apex_signal_post");
 }
 
 // ---------------------------------------------------------------- cost model
@@ -833,6 +933,10 @@ apex_status apex_decode_attention_append(apex_kv *kv, int32_t layer, const void 
 struct apex_cost {
     std::vector<double> batch, kv, us;   // us[i * nk + j]
 };
+
+namespace {
+constexpr size_t kMaxCostGrid = 256;     // grid points per axis (apex_cost_observe may add lines)
+}
 
 namespace {
 // (cell, fraction) of x on a strictly increasing grid, clamped to its ends
@@ -879,6 +983,84 @@ apex_status apex_predict_time(const apex_cost *c, int32_t batch, int64_t kv_toke
     const double u00 = c->us[i * nk + j], u10 = c->us[i1 * nk + j];
     const double u01 = c->us[i * nk + j1], u11 = c->us[i1 * nk + j1];
     *us_out = (1 - fx) * (1 - fy) * u00 + fx * (1 - fy) * u10 + (1 - fx) * fy * u01 + fx * fy * u11;
+    return APEX_OK;
+}
+
+// Online recalibration (§6; reading c17): grid lines through an
+// outside point (valued at the current clamped predictions, so no prediction changes),
+// then a normalised LMS step on the point's cell corners: prediction at the point
+// becomes exactly predicted + alpha * (measured - predicted).
+apex_status apex_cost_observe(apex_cost *c, int32_t batch, int64_t kv_tokens, double measured_us, double alpha) {
+    if (!c) return fail(APEX_EINVAL, "cost is NULL");
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(APEX_EINVAL, "alpha %g not in (0, 1]", alpha);
+    if (!std::isfinite(measured_us) || measured_us <= 0.0)
+        return fail(APEX_EINVAL, "measured_us %g must be finite and > 0", measured_us);
+    const double x = (double)batch, y = (double)kv_tokens;
+    const bool out_x = x < c->batch.front() || x > c->batch.back();
+    const bool out_y = y < c->kv.front() || y > c->kv.back();
+    if ((out_x && c->batch.size() >= kMaxCostGrid) || (out_y && c->kv.size() >= kMaxCostGrid))
+        return fail(APEX_EINVAL, "cost grid is full (%d points per axis)", kMaxCostGrid);
+    apex_cost n = *c;   // work on a copy: all-or-nothing
+    double pred = 0.0;
+    if (out_x) {
+        const size_t nk = n.kv.size(), at = x < n.batch.front() ? 0 : n.batch.size();
+        std::vector<double> row(nk);
+        for (size_t j = 0; j < nk; ++j) apex_predict_time(&n, batch, (int64_t)n.kv[j], &row[j]);
+        n.batch.insert(n.batch.begin() + at, x);
+        n.us.insert(n.us.begin() + at * nk, row.begin(), row.end());
+    }
+    if (out_y) {
+        const size_t nb = n.batch.size(), nk = n.kv.size(), at = y < n.kv.front() ? 0 : nk;
+        std::vector<double> col(nb), us;
+        for (size_t i = 0; i < nb; ++i) apex_predict_time(&n, (int32_t)n.batch[i], kv_tokens, &col[i]);
+        us.reserve(nb * (nk + 1));
+        for (size_t i = 0; i < nb; ++i) {
+            us.insert(us.end(), n.us.begin() + i * nk, n.us.begin() + i * nk + at);
+            us.push_back(col[i]);
+            us.insert(us.end(), n.us.begin() + i * nk + at, n.us.begin() + (i + 1) * nk);
+        }
+        n.kv.insert(n.kv.begin() + at, y);
+        n.us.swap(us);
+    }
+    apex_predict_time(&n, batch, kv_tokens, &pred);
+    const double e = measured_us - pred;
+    size_t i, j;
+    double fx, fy;
+    locate(n.batch, x, i, fx);
+    locate(n.kv, y, j, fy);
+    const size_t nk = n.kv.size();
+    const size_t i1 = std::min(i + 1, n.batch.size() - 1), j1 = std::min(j + 1, nk - 1);
+    // corners with their bilinear weights; coincident corners (1-point axis) merged
+    size_t idx[4] = {i * nk + j, i1 * nk + j, i * nk + j1, i1 * nk + j1};
+    double w[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < a; ++b)
+            if (idx[b] == idx[a] && w[a] != 0.0) {
+                w[b] += w[a];
+                w[a] = 0.0;
+            }
+    double norm = 0.0;
+    for (int a = 0; a < 4; ++a) norm += w[a] * w[a];
+    for (int a = 0; a < 4; ++a)
+        if (w[a] != 0.0) n.us[idx[a]] += alpha * e * w[a] / norm;
+    *c = std::move(n);
+    return APEX_OK;
+}
+
+apex_status apex_cost_size(const apex_cost *c, int32_t *nb, int32_t *nk) {
+    if (!c) return fail(APEX_EINVAL, "cost is NULL");
+    if (nb) *nb = (int32_t)c->batch.size();
+    if (nk) *nk = (int32_t)c->kv.size();
+    return APEX_OK;
+}
+
+apex_status apex_cost_table(const apex_cost *c, int32_t *batch, int64_t *kv_tokens, double *us) {
+    if (!c) return fail(APEX_EINVAL, "cost is NULL");
+    if (batch)
+        for (size_t i = 0; i < c->batch.size(); ++i) batch[i] = (int32_t)c->batch[i];
+    if (kv_tokens)
+        for (size_t j = 0; j < c->kv.size(); ++j) kv_tokens[j] = (int64_t)c->kv[j];
+    if (us) std::memcpy(us, c->us.data(), sizeof(double) * c->us.size());
     return APEX_OK;
 }
 

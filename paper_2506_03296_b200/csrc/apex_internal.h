@@ -57,8 +57,16 @@ struct DecodeParams {
     const void *q;             // [B][Hq][D]
     void *out[8];              // n_out destinations (local and/or peer-mapped), each written identically
     int64_t out_row_stride;    // elements between consecutive batch rows of a destination
-    int32_t out_head_offset;   // head index of this handle's q-head 0 inside a destination row
+    int64_t out_head_stride;   // elements between consecutive heads (D: row-major [B][H][D]; B*D: head-major)
+    int32_t out_head_offset;   // head index of this handle's q-head 0 inside a destination
     int32_t n_out;
+    // completion signal (f3): when signals[0] != nullptr, after every output row of the
+    // call is stored in every destination, signals[i][signal_slot] = signal_value
+    // (system-scope release) for i < n_out; sig_counter counts finished CTAs (left at 0)
+    uint32_t *signals[8];
+    int32_t signal_slot;
+    uint32_t signal_value;
+    int32_t *sig_counter;
     const int32_t *block_table;
     const WorkItem *items;
     const MergeItem *merges;   // unused (the kernels derive the list from hdr->o_merges)
@@ -89,6 +97,9 @@ struct TmaMap {
     CUtensorMap kv;            // 64-byte aligned opaque descriptor of one layer's KV pool
 };
 
+// sets the thread-local apex_last_error() text and returns st
+apex_status set_error(apex_status st, const char *fmt, ...);
+
 // launchers: return cudaSuccess or the launch error
 cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
                                 int32_t *block_table, int32_t *seq_lens, cudaStream_t s);
@@ -97,6 +108,12 @@ cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, v
                           cudaStream_t s);
 cudaError_t launch_decode(apex_dtype dt, int group, const TmaMap &tm, const DecodeParams &p,
                           int grid, cudaStream_t s);
+// completion signals (signal.cu): wait until every signals[i] >= value (i < n), or post
+// value into slot `slot` of each of the n_dst arrays; `status` (device, may be null)
+// receives 1 if the wait gave up after timeout_ns
+cudaError_t launch_signal_wait(const uint32_t *signals, int n, uint32_t value, uint64_t timeout_ns,
+                               uint32_t *status, cudaStream_t s);
+cudaError_t launch_signal_post(uint32_t *const *dst, int n_dst, int slot, uint32_t value, cudaStream_t s);
 // persistent-grid size the decode kernel of (dtype, group) runs with on this device
 int decode_grid_ctas(apex_dtype dt, int group, int sm_count);
 bool decode_supported(apex_dtype dt, int group);

@@ -230,9 +230,30 @@ template <int DT> __device__ __forceinline__ void store4(void *out, size_t idx, 
 template <int DT>
 __device__ __forceinline__ void store_out(const DecodeParams &p, int b, int head, int d4, float a, float bb, float c,
                                           float d) {
-    const size_t o = (size_t)b * p.out_row_stride + (size_t)(p.out_head_offset + head) * kHeadDim + d4;
+    const size_t o = (size_t)b * p.out_row_stride + (size_t)(p.out_head_offset + head) * p.out_head_stride + d4;
 #pragma unroll 1
     for (int i = 0; i < p.n_out; ++i) store4<DT>(p.out[i], o, a, bb, c, d);
+}
+
+// Completion signal.  Called by every thread of every CTA after
+// its last output store: one thread per CTA makes the CTA's stores (local or peer-mapped)
+// visible system-wide and counts the CTA; the last CTA of the grid writes signal_value
+// into every destination's signal slot with a system-scope release, then re-arms the
+// counter.  A reader that acquires the flag (apex_signal_wait) sees all the rows.
+__device__ __forceinline__ void signal_done(const DecodeParams &p) {
+    if (p.signals[0] == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        if (atomicAdd(p.sig_counter, 1) == (int)gridDim.x - 1) {
+            *p.sig_counter = 0;
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int i = 0; i < p.n_out; ++i)
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.signals[i] + p.signal_slot),
+                             "r"(p.signal_value)
+                             : "memory");
+        }
+    }
 }
 
 // this step's merge list (packed upload: right after the work items, offset in the header)
@@ -884,6 +905,14 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         }
         if (threadIdx.x == 32) TRACE(11);
     }
+    // one launch per call (fused merge): this kernel stored every output row.  Otherwise
+    // the merge kernel signals; this kernel's rows are flushed by its completion.
+    if (FUSE) {
+        signal_done(p);
+    } else if (p.signals[0] != nullptr) {
+        __syncthreads();   // this CTA's (possibly peer-mapped) rows before the merge kernel's signal
+        if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
 }
 
 // log-sum-exp merge of split pairs as its own launch (bandwidth regime): one CTA
@@ -902,6 +931,7 @@ __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeP
     for (int i = blockIdx.x; i < n; i += gridDim.x)
         merge_pair<DT, G>(p, merges_of(p)[i], threadIdx.x, blockDim.x, red, redml, kMergeThreads,
                           [] { __syncthreads(); });
+    signal_done(p);   // runs after the decode grid completed (griddepcontrol.wait): all rows stored
 }
 
 template <int DT, int G> cudaError_t prepare() {

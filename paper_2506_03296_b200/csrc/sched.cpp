@@ -14,14 +14,19 @@ extern "C" {
 
 // Eq6: N_G/N_C < 2 T_glinear/T_gatt + 3 + T_gatt/T_glinear
 apex_status apex_pipelining_threshold(double t_glinear, double t_gatt, double *out) {
-    if (!out || !pos(t_glinear) || !pos(t_gatt)) return APEX_EINVAL;
+    if (!out) return apex::set_error(APEX_EINVAL, "apex_pipelining_threshold: out is NULL");
+    if (!pos(t_glinear) || !pos(t_gatt))
+        return apex::set_error(APEX_EINVAL, "apex_pipelining_threshold: T_glinear %g and T_gatt %g must be finite and > 0",
+                               t_glinear, t_gatt);
     *out = 2.0 * t_glinear / t_gatt + 3.0 + t_gatt / t_glinear;
     return APEX_OK;
 }
 
 apex_status apex_decide(const apex_sched_input *in, apex_decision *out) {
-    if (!in || !out) return APEX_EINVAL;
-    if (in->n_prefill < 0 || in->n_gpu_decode < 0 || in->n_cpu_decode < 0) return APEX_EINVAL;
+    if (!in || !out) return apex::set_error(APEX_EINVAL, "apex_decide: in/out is NULL");
+    if (in->n_prefill < 0 || in->n_gpu_decode < 0 || in->n_cpu_decode < 0)
+        return apex::set_error(APEX_EINVAL, "apex_decide: negative request count (%d, %d, %d)", in->n_prefill,
+                               in->n_gpu_decode, in->n_cpu_decode);
     *out = apex_decision{APEX_STRATEGY_GPU_ONLY, 0, 0.0, 0.0, 0.0};
     // Alg. 1 lines 4-6: no requests designated for CPU offload -> GPU-only
     if (in->n_cpu_decode == 0) return APEX_OK;
@@ -30,7 +35,8 @@ apex_status apex_decide(const apex_sched_input *in, apex_decision *out) {
         out->gate_closed = 1;
         return APEX_OK;
     }
-    if (!pos(in->n_g) || !pos(in->n_c) || !pos(in->t_glinear) || !pos(in->t_gatt)) return APEX_EINVAL;
+    if (!pos(in->n_g) || !pos(in->n_c) || !pos(in->t_glinear) || !pos(in->t_gatt))
+        return apex::set_error(APEX_EINVAL, "apex_decide: N_G, N_C, T_glinear, T_gatt must be finite and > 0");
     const double ng = in->n_g, nc = in->n_c, tl = in->t_glinear, ta = in->t_gatt;
     const double rhs = ng * ta / (tl + ta);                     // GPU-only throughput (Eq5 right side)
     double lhs;
@@ -39,7 +45,9 @@ apex_status apex_decide(const apex_sched_input *in, apex_decision *out) {
         lhs = (ng * ta + nc * (2.0 * tl + ta)) / (2.0 * tl + ta);
         apex_pipelining_threshold(tl, ta, &out->eq6_threshold);
     } else {
-        if (!pos(in->t_glinear_pref) || !pos(in->t_gatt_pref)) return APEX_EINVAL;
+        if (!pos(in->t_glinear_pref) || !pos(in->t_gatt_pref))
+            return apex::set_error(APEX_EINVAL, "apex_decide: T_glinear_pref and T_gatt_pref must be finite and > 0 "
+                                                "when n_prefill > 0");
         // mixed (Alg. 1 lines 20-23): N_Ctotal = N_C (T_glinear_pref + T_glinear + T_gatt_pref),
         // compared over the same (2 T_glinear + T_gatt) window as printed
         const double t_ov = in->t_glinear_pref + tl + in->t_gatt_pref;

@@ -7,6 +7,7 @@ runs the allocator/planner without any CUDA call (CPU tests, sharding logic).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 
@@ -57,13 +58,14 @@ class PagedKVCache:
         self.seq_lens = torch.zeros((max_seqs,), dtype=torch.int32, device=self.device)
         desc.kv_pool = (ctypes.c_void_p * num_layers)(*[t.data_ptr() for t in self.kv_pools])
         desc.block_table, desc.seq_lens = self.block_table.data_ptr(), self.seq_lens.data_ptr()
-        nbytes = A.apex_kv_workspace_bytes(desc)
-        if nbytes == 0:
-            # surface the validation message
-            A.apex_kv_create(desc)
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        desc.workspace, desc.workspace_bytes = self.workspace.data_ptr(), nbytes
-        self.handle = A.apex_kv_create(desc)
+        with torch.cuda.device(self.device):
+            nbytes = A.apex_kv_workspace_bytes(desc)
+            if nbytes == 0:
+                # surface the validation message
+                A.apex_kv_create(desc)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            desc.workspace, desc.workspace_bytes = self.workspace.data_ptr(), nbytes
+            self.handle = A.apex_kv_create(desc)
 
     # -- lifecycle
     def close(self):
@@ -80,9 +82,18 @@ class PagedKVCache:
     def _stream(self) -> int:
         return 0 if self.host_only else _stream_ptr(self.device)
 
+    def _on_device(self):
+        """Make this cache's GPU current for an ABI call (the library uses the current
+        device for attributes, memsets and the SM count)."""
+        if self.host_only:
+            return contextlib.nullcontext()
+        import torch
+        return torch.cuda.device(self.device)
+
     # -- step API (names follow the C ABI)
     def alloc(self, seq_ids, n_new):
-        A.apex_kv_alloc(self.handle, seq_ids, n_new, self._stream())
+        with self._on_device():
+            A.apex_kv_alloc(self.handle, seq_ids, n_new, self._stream())
         self.batch_seq_ids = [int(s) for s in seq_ids]
         self.n_rows = int(sum(int(x) for x in n_new))
 
@@ -92,7 +103,8 @@ class PagedKVCache:
     def append(self, layer: int, k_new, v_new):
         self._check_rows(k_new, self.n_rows, self.num_kv_heads)
         self._check_rows(v_new, self.n_rows, self.num_kv_heads)
-        A.apex_kv_append(self.handle, layer, k_new.data_ptr(), v_new.data_ptr(), self._stream())
+        with self._on_device():
+            A.apex_kv_append(self.handle, layer, k_new.data_ptr(), v_new.data_ptr(), self._stream())
 
     def decode(self, layer: int, q, out=None, scale: float | None = None):
         import torch
@@ -104,7 +116,8 @@ class PagedKVCache:
             self._check_rows(out, B, self.num_q_heads)
         if scale is None:
             scale = 1.0 / math.sqrt(self.head_dim)
-        A.apex_decode_attention(self.handle, layer, q.data_ptr(), out.data_ptr(), scale, self._stream())
+        with self._on_device():
+            A.apex_decode_attention(self.handle, layer, q.data_ptr(), out.data_ptr(), scale, self._stream())
         return out
 
     def decode_append(self, layer: int, q, k_new, v_new, out=None, scale: float | None = None):
@@ -121,25 +134,55 @@ class PagedKVCache:
             self._check_rows(out, B, self.num_q_heads)
         if scale is None:
             scale = 1.0 / math.sqrt(self.head_dim)
-        A.apex_decode_attention_append(self.handle, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
-                                       out.data_ptr(), scale, self._stream())
+        with self._on_device():
+            A.apex_decode_attention_append(self.handle, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                                           out.data_ptr(), scale, self._stream())
         return out
 
-    def decode_into(self, layer: int, q, outs, head_offset: int = 0, scale: float | None = None):
-        """Decode writing this handle's q heads into each full-width [B][H_total][D] tensor of
-        `outs` at head `head_offset` (fused all-gather epilogue when `outs` are peer-mapped
-        symmetric buffers of the other ranks)."""
+    def decode_into(self, layer: int, q, outs, head_offset: int = 0, layout: str = "bhd", scale: float | None = None,
+                    signals=None, signal_slot: int = 0, signal_value: int = 0):
+        """Decode writing this handle's q heads into each tensor of `outs` at head `head_offset`.
+
+        layout "bhd": outs are [B][H_total][D] (row-major); "hbd": [H_total][B][D]
+        (head-major: a rank's head slice is contiguous, so an NCCL all-gather of
+        [Hq/N][B][D] slices yields [Hq][B][D] with no permute).  All outs must have the
+        same shape and dtype.  With peer-mapped symmetric buffers of the other ranks as
+        `outs` the all-gather happens in the epilogue (f3); `signals` (one uint32 tensor
+        or pointer per destination) then receive `signal_value` at `signal_slot` once
+        every row is stored (in-kernel completion flag)."""
         B = len(self.batch_seq_ids)
         self._check_rows(q, B, self.num_q_heads)
+        if not outs:
+            raise ValueError("outs is empty")
+        shape = tuple(outs[0].shape)
+        want_dt = torch_dtype(self.dtype)
         for o in outs:
-            if o.dim() != 3 or o.shape[0] != B or o.shape[2] != self.head_dim or not o.is_contiguous() \
-                    or o.dtype != torch_dtype(self.dtype):
-                raise ValueError("outs must be contiguous [B][H_total][D] tensors of the cache dtype")
+            if (tuple(o.shape) != shape or o.dim() != 3 or not o.is_contiguous() or o.dtype != want_dt
+                    or o.device != self.device):
+                raise ValueError("outs must be contiguous 3-D tensors of one shape and the cache dtype")
+        if layout == "bhd":
+            h_total = shape[1]
+            if shape[0] != B or shape[2] != self.head_dim:
+                raise ValueError(f"bhd outs must be [B={B}][H][{self.head_dim}], got {shape}")
+            row_stride, head_stride = h_total * self.head_dim, self.head_dim
+        elif layout == "hbd":
+            h_total = shape[0]
+            if shape[1] != B or shape[2] != self.head_dim:
+                raise ValueError(f"hbd outs must be [H][B={B}][{self.head_dim}], got {shape}")
+            row_stride, head_stride = self.head_dim, B * self.head_dim
+        else:
+            raise ValueError(f"unknown layout {layout!r}")
+        if head_offset < 0 or head_offset + self.num_q_heads > h_total:
+            raise ValueError(f"heads [{head_offset}, {head_offset + self.num_q_heads}) exceed H_total={h_total}")
         if scale is None:
             scale = 1.0 / math.sqrt(self.head_dim)
-        stride = outs[0].shape[1] * self.head_dim
-        A.apex_decode_attention_ex(self.handle, layer, q.data_ptr(), [o.data_ptr() for o in outs], stride,
-                                   head_offset, scale, self._stream())
+        sig = None
+        if signals is not None:
+            sig = [x if isinstance(x, int) else x.data_ptr() for x in signals]
+        with self._on_device():
+            A.apex_decode_attention_ex(self.handle, layer, q.data_ptr(), [o.data_ptr() for o in outs], row_stride,
+                                       head_stride, head_offset, scale, self._stream(), sig, signal_slot,
+                                       signal_value)
 
     def _check_rows(self, t, rows, heads):
         if t.device != self.device or t.dtype != torch_dtype(self.dtype) or not t.is_contiguous():

@@ -70,3 +70,51 @@ def test_eq1_to_eq4_and_fig_b_rates():
     f = G["fig_b_rates"]
     assert f["kv_tokens"] / f["gpu_us"] == pytest.approx(f["n_g_tokens_per_us"], rel=1e-15)
     assert f["cpu_us"] / f["gpu_us"] == pytest.approx(f["ng_over_nc"], rel=1e-15)
+
+
+# ---- online recalibration (reading c17)
+
+GO = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cost_observe_pins.json")))
+
+
+def test_observe_hand_derived_pins():
+    for c in GO["cases"]:
+        b, k = c["point"]
+        bg, kg, us = cm.observe(GO["batch_grid"], GO["kv_grid"], GO["us"], b, k, c["measured"], c["alpha"])
+        assert bg == c["batch_grid"] and kg == c["kv_grid"], c["what"]
+        for row, want in zip(us, c["us"]):
+            assert row == pytest.approx(want, abs=1e-12), c["what"]
+
+
+def test_observe_properties():
+    """Invariants of reading c17 on random tables: the input table is untouched; after one
+    step the prediction at the point is pred + alpha*e; predictions outside the point's
+    cell (and everywhere, for the grid-line insertion alone) are unchanged."""
+    rnd = random.Random(11)
+    for _ in range(200):
+        nb, nk = rnd.randint(1, 4), rnd.randint(1, 4)
+        bg = sorted(rnd.sample(range(1, 500), nb))
+        kg = sorted(rnd.sample(range(1, 10 ** 6), nk))
+        us = [[rnd.uniform(1, 1000) for _ in kg] for _ in bg]
+        snap = [row[:] for row in us]
+        b, k = rnd.randint(0, 600), rnd.randint(0, 2 * 10 ** 6)
+        m, a = rnd.uniform(1, 2000), rnd.choice([1.0, 0.5, 0.1])
+        pred = cm.interp(bg, kg, us, b, k)
+        bg2, kg2, us2 = cm.observe(bg, kg, us, b, k, m, a)
+        assert us == snap
+        assert cm.interp(bg2, kg2, us2, b, k) == pytest.approx(pred + a * (m - pred), rel=1e-9, abs=1e-9)
+        # probes whose cell shares no corner with the point's cell keep their predictions
+        def corners(x, y):
+            i, _ = cm._axis(bg2, x)
+            j, _ = cm._axis(kg2, y)
+            return {(a, c) for a in (i, min(i + 1, len(bg2) - 1)) for c in (j, min(j + 1, len(kg2) - 1))}
+        mine = corners(b, k)
+        for _ in range(20):
+            pb, pk = rnd.randint(0, 600), rnd.randint(0, 2 * 10 ** 6)
+            if corners(pb, pk) & mine:
+                continue
+            assert cm.interp(bg2, kg2, us2, pb, pk) == pytest.approx(cm.interp(bg, kg, us, pb, pk), rel=1e-9)
+    with pytest.raises(ValueError):
+        cm.observe([1], [1], [[1.0]], 1, 1, 1.0, 0.0)
+    with pytest.raises(ValueError):
+        cm.observe([1], [1], [[1.0]], 1, 1, -1.0, 1.0)

@@ -70,7 +70,10 @@ def _worker(rank, world, port, mode, result_path):
         ks = [synth.gen_seq(1, 0, b, c, kv_hi - kv_lo, D, "bf16", head_offset=kv_lo) for b, c in enumerate(ctx)]
         vs = [synth.gen_seq(2, 0, b, c, kv_hi - kv_lo, D, "bf16", head_offset=kv_lo) for b, c in enumerate(ctx)]
         local = torch.from_numpy(oa.decode_attention(q, ks, vs, "bf16", nthreads=1))
-        full = gather_heads(local)
+        # head-major [Hq/N][B][D] slices gather into [Hq][B][D] with no permute
+        full = gather_heads(local.permute(1, 0, 2).contiguous())
+        assert full.shape == (Hq, B, D)
+        full = full.permute(1, 0, 2)
         # the rank's planner over its head slice covers exactly its kv heads
         cache = PagedKVCache(num_layers=1, num_q_heads=q_hi - q_lo, num_kv_heads=kv_hi - kv_lo, num_blocks=64,
                              max_seqs=B, max_blocks_per_seq=16, max_batch=B, max_new_tokens=1024, host_only=True)
