@@ -27,7 +27,7 @@ EXPORTS = ["apex_kv_workspace_bytes", "apex_kv_create", "apex_kv_destroy", "apex
            "apex_cost_create", "apex_predict_time", "apex_cost_destroy", "apex_last_error", "apex_version",
            "apex_synth_rows", "apex_pipelining_threshold", "apex_decide", "apex_kv_decode_launches", "apex_decode_attention_ex",
            "apex_decode_attention_append", "apex_signal_wait", "apex_signal_post", "apex_cost_observe",
-           "apex_cost_size", "apex_cost_table"]
+           "apex_cost_size", "apex_cost_table", "apex_kv_set_planner"]
 STRATEGIES = {0: "gpu_only", 1: "asym_pipeline", 2: "async_overlap"}
 
 
@@ -99,6 +99,7 @@ def lib():
             "apex_decode_attention_ex": (c_int, [c_void_p, c_int32, c_void_p, POINTER(c_void_p), c_int32, c_int64,
                                                  c_int64, c_int32, POINTER(c_void_p), c_int32, c_uint32, c_float,
                                                  c_void_p]),
+            "apex_kv_set_planner": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32]),
             "apex_cost_observe": (c_int, [c_void_p, c_int32, c_int64, c_double, c_double]),
             "apex_cost_size": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32)]),
             "apex_cost_table": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -176,6 +177,12 @@ def apex_kv_set_grid(kv: int, ctas: int) -> None:
 
 def apex_kv_set_sched(kv: int, dyn_permille: int) -> None:
     _check(lib().apex_kv_set_sched(kv, int(dyn_permille)))
+
+
+def apex_kv_set_planner(kv: int, latency_tiles_per_cta: int = 512, guided_div: int = 8, guided_pm1: int = 900,
+                        guided_pm2: int = 950, guided_pm3: int = 980) -> None:
+    _check(lib().apex_kv_set_planner(kv, int(latency_tiles_per_cta), int(guided_div), int(guided_pm1),
+                                     int(guided_pm2), int(guided_pm3)))
 
 
 def apex_kv_num_free_blocks(kv: int) -> int:

@@ -103,7 +103,7 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     // block-table deltas, length deltas (packed)]; the kernels' pointers into it never move
     // header | cta_begin[grid + 1] (grid <= 4 * SMs) | items ...
     w.o_items = align_up(apex::kCtaBeginOffset + sizeof(int32_t) * (4 * (size_t)sm_count + 1), 256);
-    w.o_merges = w.o_items + align_up(sizeof(WorkItem) * (size_t)w.max_items, 256);
+    w.o_merges = w.o_items + align_up(sizeof(apex::ItemRec) * (size_t)w.max_items, 256);
     w.o_tail = w.o_merges + align_up(sizeof(MergeItem) * (size_t)w.max_merges, 256);
     size_t up = w.o_tail;
     up += align_up(sizeof(int32_t) * (size_t)d->max_new_tokens, 256);
@@ -357,6 +357,23 @@ apex_status apex_kv_set_sched(apex_kv *kv, int32_t dyn_permille) {
     if (!kv || dyn_permille < -2 || dyn_permille > 1000)
         return fail(APEX_EINVAL, "dyn_permille %d not in [-2, 1000]", dyn_permille);
     kv->dyn_permille = dyn_permille;
+    return APEX_OK;
+}
+
+apex_status apex_kv_set_planner(apex_kv *kv, int32_t latency_tiles_per_cta, int32_t guided_div, int32_t guided_pm1,
+                                int32_t guided_pm2, int32_t guided_pm3) {
+    if (!kv) return fail(APEX_EINVAL, "kv is NULL");
+    if (latency_tiles_per_cta < 0 || latency_tiles_per_cta > (1 << 20))
+        return fail(APEX_EINVAL, "latency_tiles_per_cta %d not in [0, 2^20]", latency_tiles_per_cta);
+    if (guided_div < 1 || guided_div > 64) return fail(APEX_EINVAL, "guided_div %d not in [1, 64]", guided_div);
+    if (!(0 <= guided_pm1 && guided_pm1 <= guided_pm2 && guided_pm2 <= guided_pm3 && guided_pm3 <= 1000))
+        return fail(APEX_EINVAL, "guided permilles must satisfy 0 <= %d <= %d <= %d <= 1000", guided_pm1, guided_pm2,
+                    guided_pm3);
+    kv->latency_tiles_per_cta = latency_tiles_per_cta;
+    kv->guided[0] = guided_div;
+    kv->guided[1] = guided_pm1;
+    kv->guided[2] = guided_pm2;
+    kv->guided[3] = guided_pm3;
     return APEX_OK;
 }
 
@@ -657,7 +674,7 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     // packed upload: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
     // len deltas -- one H2D copy of exactly the used bytes; kernels find the merge list and
     // the slot map through offsets in the header (fixed launch parameters)
-    const size_t items_bytes = sizeof(WorkItem) * plan.items.size();
+    const size_t items_bytes = sizeof(apex::ItemRec) * plan.items.size();
     const size_t merges_bytes = sizeof(MergeItem) * plan.merges.size();
     const size_t o_merges = align_up(kv->ws.o_items + items_bytes, 256);
     const size_t o_slots = o_merges + align_up(merges_bytes, 256);
@@ -722,7 +739,15 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         hdr.o_slots = (int32_t)o_slots;
         std::memcpy(host, &hdr, sizeof hdr);
         std::memcpy(host + apex::kCtaBeginOffset, plan.cta_begin.data(), sizeof(int32_t) * plan.cta_begin.size());
-        if (items_bytes) std::memcpy(host + kv->ws.o_items, plan.items.data(), items_bytes);
+        // items + the physical ids of their first blocks (known now that the blocks are popped)
+        apex::ItemRec *rec = reinterpret_cast<apex::ItemRec *>(host + kv->ws.o_items);
+        for (size_t t = 0; t < plan.items.size(); ++t) {
+            const WorkItem &it = plan.items[t];
+            const std::vector<int32_t> &blocks = kv->seqs[it.seq].blocks;
+            rec[t].it = it;
+            for (int u = 0; u < apex::kInlineIds; ++u)
+                rec[t].ids[u] = u < it.nblk ? blocks[(size_t)it.blk0 + u] : -1;
+        }
         if (merges_bytes) std::memcpy(host + o_merges, plan.merges.data(), merges_bytes);
         if (rows) std::memcpy(host + o_slots, slots.data(), sizeof(int32_t) * slots.size());
         if (need) std::memcpy(host + o_bt, bt_delta.data(), sizeof(int2) * bt_delta.size());
@@ -844,7 +869,7 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
     uint8_t *up = ws + kv->ws.upload;
     p.hdr = (const apex::StepHeader *)up;
     p.cta_begin = (const int32_t *)(up + apex::kCtaBeginOffset);
-    p.items = (const WorkItem *)(up + kv->ws.o_items);
+    p.items = (const apex::ItemRec *)(up + kv->ws.o_items);
     p.merges = nullptr;                 // device side: hdr->o_merges (packed upload)
     p.part_o = (float *)(ws + kv->ws.part_o);
     p.part_ml = (float *)(ws + kv->ws.part_ml);

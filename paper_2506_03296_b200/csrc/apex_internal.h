@@ -28,6 +28,15 @@ struct __align__(16) WorkItem {
     int32_t mg;       // index into the merge list (split items), or -1
 };
 
+// A work item as uploaded: the item plus the physical ids of its first kInlineIds
+// blocks (-1 past nblk), so the producer can issue the first TMA loads in the same
+// round trip as the item instead of after a dependent block-table load.
+constexpr int kInlineIds = 8;
+struct __align__(16) ItemRec {
+    WorkItem it;
+    int32_t ids[kInlineIds];
+};
+
 // One (b, g) pair whose items were split: partial slots [part0, part0+nparts).
 // The last item of the pair to finish merges the partials inside the decode kernel.
 struct __align__(16) MergeItem {
@@ -68,7 +77,7 @@ struct DecodeParams {
     uint32_t signal_value;
     int32_t *sig_counter;
     const int32_t *block_table;
-    const WorkItem *items;
+    const ItemRec *items;
     const MergeItem *merges;   // unused (the kernels derive the list from hdr->o_merges)
     float *part_o;             // [slots][G][D]   unnormalised sum_t p_t v_t (fp32)
     float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)

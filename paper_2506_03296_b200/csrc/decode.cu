@@ -345,6 +345,9 @@ template <int DT> struct SimtConsumer {
         // ---- s_t (log2 units): lane t, dims of half hh
         float acc = 0.f;
         if constexpr (F32) {
+            // four independent FMA chains (16 deep instead of 64): in the latency regime a
+            // warp usually holds one tile, so the dependent-FMA latency is on the critical path
+            float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int sg = 0; sg < 2; ++sg) {
                 const uint32_t rowa = kt + (uint32_t)((2 * hh + sg) * kSegStride + t * 128);
@@ -352,12 +355,13 @@ template <int DT> struct SimtConsumer {
                 for (int c = 0; c < 8; ++c) {
                     uint4 k4 = lds128(rowa + ((c ^ t7) << 4));
                     const float *qq = qv + sg * 32 + c * 4;
-                    acc = fmaf(qq[0], __uint_as_float(k4.x), acc);
-                    acc = fmaf(qq[1], __uint_as_float(k4.y), acc);
-                    acc = fmaf(qq[2], __uint_as_float(k4.z), acc);
-                    acc = fmaf(qq[3], __uint_as_float(k4.w), acc);
+                    a4[0] = fmaf(qq[0], __uint_as_float(k4.x), a4[0]);
+                    a4[1] = fmaf(qq[1], __uint_as_float(k4.y), a4[1]);
+                    a4[2] = fmaf(qq[2], __uint_as_float(k4.z), a4[2]);
+                    a4[3] = fmaf(qq[3], __uint_as_float(k4.w), a4[3]);
                 }
             }
+            acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         } else {
             const uint32_t rowa = kt + (uint32_t)(hh * kSegStride + t * 128);
 #pragma unroll
@@ -388,16 +392,19 @@ template <int DT> struct SimtConsumer {
         }
         // ---- O += p_r V_r over lane-owned dims
         if constexpr (F32) {
+            // even rows accumulate into o[0..3], odd rows into o[4..7] (two chains of 8; the
+            // halves are added in finish())
             const int sg = lane >> 3, c = lane & 7;
-#pragma unroll 4
+#pragma unroll
             for (int r = 0; r < kTileRows; ++r) {
                 const float pr = __shfl_sync(0xffffffffu, pt, r);
                 if (r < valid) {
                     uint4 v4 = lds128(vt + (uint32_t)(sg * kSegStride + r * 128) + ((c ^ (r & 7)) << 4));
-                    o[0] = fmaf(pr, __uint_as_float(v4.x), o[0]);
-                    o[1] = fmaf(pr, __uint_as_float(v4.y), o[1]);
-                    o[2] = fmaf(pr, __uint_as_float(v4.z), o[2]);
-                    o[3] = fmaf(pr, __uint_as_float(v4.w), o[3]);
+                    float *oo = o + 4 * (r & 1);
+                    oo[0] = fmaf(pr, __uint_as_float(v4.x), oo[0]);
+                    oo[1] = fmaf(pr, __uint_as_float(v4.y), oo[1]);
+                    oo[2] = fmaf(pr, __uint_as_float(v4.z), oo[2]);
+                    oo[3] = fmaf(pr, __uint_as_float(v4.w), oo[3]);
                 }
             }
         } else {
@@ -427,7 +434,8 @@ template <int DT> struct SimtConsumer {
         float *dst = cb_o + (size_t)wc * kHeadDim;
         if constexpr (F32) {
             const int sg = lane >> 3, c = lane & 7;
-            *reinterpret_cast<float4 *>(dst + sg * 32 + c * 4) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4 *>(dst + sg * 32 + c * 4) =
+                make_float4(o[0] + o[4], o[1] + o[5], o[2] + o[6], o[3] + o[7]);
         } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(0xffffffffu, o[i], 16);
@@ -731,7 +739,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // speculative load of item blockIdx.x (the first item of CTA i is item i unless the
         // plan has stream-K ranges): issued together with the header loads, one round
         // trip earlier than a load that waits for cta_begin (the list has >= grid slots)
-        const WorkItem spec = p.items[blockIdx.x];
+        const WorkItem spec = p.items[blockIdx.x].it;
+        const int spec_ids = lane < kInlineIds ? p.items[blockIdx.x].ids[lane] : 0;
         int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
 #pragma unroll
         for (int q = 0; q < NC; ++q) pc[q] = 0;
@@ -753,7 +762,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 break;
             }
-            const WorkItem it = (APEX_SPEC_ITEM && k == 0 && idx == (int)blockIdx.x) ? spec : p.items[idx];
+            const bool use_spec = APEX_SPEC_ITEM && k == 0 && idx == (int)blockIdx.x;
+            const WorkItem it = use_spec ? spec : p.items[idx].it;
+            // physical ids of the item's first kInlineIds blocks, loaded with the item: the
+            // first TMAs do not wait for the dependent block-table load below
+            const int inl = use_spec ? spec_ids : (lane < kInlineIds ? p.items[idx].ids[lane] : 0);
             if (lane == 0) {
                 ring[slot].it = it;
                 mbar_arrive(ifull0 + 8 * slot);
@@ -761,7 +774,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             }
             const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my = (j0 + lane < it.nblk) ? __ldg(bt + j0 + lane) : 0;
+                const int my = (j0 + lane < it.nblk && j0 + lane >= kInlineIds) ? __ldg(bt + j0 + lane) : 0;
                 const int cnt = min(32, it.nblk - j0);
 #ifdef APEX_TRACE
                 if (k == 0 && j0 == 0) {
@@ -770,7 +783,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
 #endif
                 for (int jj = 0; jj < cnt; ++jj) {
-                    const int phys = __shfl_sync(0xffffffffu, my, jj);
+                    const int phys = j0 + jj < kInlineIds ? __shfl_sync(0xffffffffu, inl, jj)
+                                                          : __shfl_sync(0xffffffffu, my, jj);
                     if (AP && it.blk0 + j0 + jj == (it.len - 1) / kTileRows)   // fused append
                         NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
                     const int w = (j0 + jj) % NC;

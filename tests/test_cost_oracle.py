@@ -118,3 +118,30 @@ def test_observe_properties():
         cm.observe([1], [1], [[1.0]], 1, 1, 1.0, 0.0)
     with pytest.raises(ValueError):
         cm.observe([1], [1], [[1.0]], 1, 1, -1.0, 1.0)
+
+
+def test_algorithm1_direct_pins():
+    """oracle.cost_model.algorithm1 pinned by itself on SPEC.md
+    S:201-239 examples and hand-evaluated Eq5 sides (Alg. 1)."""
+    a1 = cm.algorithm1
+    # S:205 N_G/N_C = 5 < Eq6 threshold 6 (T_gatt = T_glinear): lhs (5+3)/3 = 2.67 > rhs 5/2 = 2.5
+    assert a1(0, 1, 100, 5.0, 1.0, 1.0, 1.0) == "asym_pipeline"
+    # S:206 Fig. 2b ratio 3031/170 = 17.83 > 6: lhs (17.83+3)/3 = 6.94 < rhs 8.91
+    assert a1(0, 1, 100, 3031 / 170, 1.0, 1.0, 1.0) == "async_overlap"
+    # exactly at the Eq6 threshold (N_G/N_C = 6): lhs (6+3)/3 = 3 == rhs 6/2 = 3, strict ">" -> AO
+    assert a1(0, 1, 100, 6.0, 1.0, 1.0, 1.0) == "async_overlap"
+    # S:207 N_C = N_G -> AP for any positive times (ratio 1 < min threshold 2*sqrt(2)+3)
+    for tl, ta in [(0.1, 9.0), (3.0, 0.7), (1.0, 1.0)]:
+        assert a1(0, 1, 100, 2.0, 2.0, tl, ta) == "asym_pipeline"
+    # S:215 mixed with T_glinear_pref = T_glinear, T_gatt_pref = T_gatt == decode-only
+    for ng in (3.0, 5.0, 17.8):
+        assert a1(3, 1, 100, ng, 1.0, 1.0, 1.0, 1.0, 1.0) == a1(0, 1, 100, ng, 1.0, 1.0, 1.0)
+    # S:216 a long prefill window: lhs (17.8 + 42)/3 = 19.93 > rhs 8.9 -> AP
+    assert a1(3, 1, 100, 17.8, 1.0, 1.0, 1.0, 40.0, 1.0) == "asym_pipeline"
+    # S:217 N_C -> 0 in the mixed branch -> AO
+    assert a1(3, 1, 100, 17.8, 1e-12, 1.0, 1.0, 40.0, 1.0) == "async_overlap"
+    # S:221-227 ratio gate (P:378): 80 >= 8*10 passes; 79 closes; no CPU requests -> GPU-only
+    assert a1(0, 10, 80, 5.0, 1.0, 1.0, 1.0) == "asym_pipeline"
+    assert a1(0, 10, 79, 5.0, 1.0, 1.0, 1.0) == "gpu_only"
+    assert a1(0, 10, 0, 5.0, 1.0, 1.0, 1.0) == "gpu_only"
+    assert a1(0, 10, 79, 5.0, 1.0, 1.0, 1.0, min_cpu_ratio=0.0) == "asym_pipeline"

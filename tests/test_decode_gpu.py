@@ -11,7 +11,7 @@ from helpers import check_close, decode_step, gen_dev, make_cache, oracle_rows, 
 
 pytestmark = pytest.mark.gpu
 
-COMBOS = [("f32", 4, 4), ("f16", 4, 4), ("f16", 8, 2), ("f16", 16, 4), ("f16", 16, 2), ("bf16", 8, 4),
+COMBOS = [("f32", 4, 4), ("f16", 4, 4), ("f16", 8, 4), ("f16", 8, 2), ("f16", 16, 4), ("f16", 16, 2), ("bf16", 8, 4),
           ("bf16", 16, 4), ("bf16", 16, 2)]
 RAGGED = [1, 2, 15, 16, 17, 31, 64, 100, 257, 1000, 2049]
 

@@ -12,12 +12,16 @@ from helpers import check_close, gen_dev, make_cache, oracle_rows, prefill, to_f
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dtype,hq,hkv,ctx", [("bf16", 32, 8, [1, 15, 16, 17, 300, 2000]),
-                                              ("f16", 32, 32, [5, 31, 32, 1000]),
-                                              ("f32", 8, 8, [2, 16, 100]),
-                                              ("f16", 16, 2, [1, 33, 4096]),
-                                              ("bf16", 32, 8, [4096] * 40)])      # bandwidth regime
-def test_fused_append_matches_two_calls(cuda_lib, dtype, hq, hkv, ctx):
+@pytest.mark.parametrize("dtype,hq,hkv,ctx,launches", [("bf16", 32, 8, [1, 15, 16, 17, 300, 2000], 1),
+                                                       ("f16", 32, 32, [5, 31, 32, 1000], 1),
+                                                       ("f32", 8, 8, [2, 16, 100], 1),
+                                                       ("f16", 16, 2, [1, 33, 4096], 1),
+                                                       # latency regime near its edge: T = 82240 <= 512 * 296
+                                                       ("bf16", 32, 8, [4096] * 40, 1),
+                                                       # bandwidth regime: T = 40 * 513 * 8 = 164160 > 512 * 296
+                                                       # (append kernel + decode kernel + merge kernel)
+                                                       ("bf16", 32, 8, [8192] * 40, 2)])
+def test_fused_append_matches_two_calls(cuda_lib, dtype, hq, hkv, ctx, launches):
     import torch
     B, steps = len(ctx), 18                                      # crosses a 16-token block boundary
     nb = sum(-(-(c + steps) // 16) for c in ctx) + 8
@@ -36,6 +40,7 @@ def test_fused_append_matches_two_calls(cuda_lib, dtype, hq, hkv, ctx):
         q = gen_dev(fused, 0, 0, seqs, pos, hq)
         k = gen_dev(fused, 1, 0, seqs, pos, hkv)
         v = gen_dev(fused, 2, 0, seqs, pos, hkv)
+        assert fused.decode_launches() == launches, "planner regime of the case"
         out_f = fused.decode_append(0, q, k, v)
         ref.append(0, k, v)
         out_r = ref.decode(0, q)

@@ -379,3 +379,19 @@ def test_cost_observe_matches_oracle():
         assert ei.value.code == "EINVAL"
     assert A.apex_cost_table(h) == ([1], [1], [[1.0]])
     A.apex_cost_destroy(h)
+
+
+def test_set_planner_validation_and_effect():
+    c = host_cache(num_q_heads=32, num_kv_heads=8, num_blocks=8192, max_blocks_per_seq=1024, max_new_tokens=1 << 16)
+    c.set_grid(296)
+    for bad in [(-1, 8, 900, 950, 980), (512, 0, 900, 950, 980), (512, 65, 900, 950, 980),
+                (512, 8, 950, 900, 980), (512, 8, 900, 950, 1001)]:
+        with pytest.raises(A.ApexError) as ei:
+            c.set_planner(bad[0], bad[1], bad[2:])
+        assert ei.value.code == "EINVAL"
+    c.alloc([0], [16000])                   # T = 8000 tiles <= 512 * 296: latency regime
+    assert c.decode_launches() == 1
+    c.set_planner(0)                        # latency regime disabled -> bandwidth plan + merge kernel
+    c.alloc([0], [1])
+    assert c.decode_launches() == 2
+    _check_plan(c, [16001], 8)

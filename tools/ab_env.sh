@@ -1,5 +1,5 @@
 #!/bin/bash
-# Same-box A/B of an environment knob (e.g. APEX_GUIDED, APEX_LAT_TILES) with bench.py, interleaved,
+# Same-box A/B of an environment variable read by bench.py or its dependencies (the library itself reads none), interleaved,
 # under gpurun:  bash tools/ab_env.sh "<configs>" VAR "<values>"   -> gpurun_out/ab_env/
 set -u
 O=$PWD/gpurun_out/ab_env; mkdir -p $O

@@ -44,7 +44,7 @@ def main():
     es = 4 if w.dtype == "f32" else 2
     nbytes = sum(c * w.num_kv_heads * 128 * 2 * es for c in ctx) + 2 * B * w.num_q_heads * 128 * es
     res = []
-    # a sched entry "-2:8/800/900/950" sets APEX_GUIDED for the guided planner
+    # a sched entry "-2:8/800/900/950" sets the guided planner's constants (apex_kv_set_planner)
     scheds = a.scheds.split(",") if a.scheds else [None]
     for grid, chunk, sched in [(g, c, s) for g in [int(x) for x in a.grids.split(",")]
                                for c in [int(x) for x in a.chunks.split(",")] for s in scheds]:
@@ -54,7 +54,8 @@ def main():
             if sched is not None:
                 sv, _, gp = sched.partition(":")
                 if gp:
-                    os.environ["APEX_GUIDED"] = gp.replace("/", ",")
+                    div, p1, p2, p3 = [int(x) for x in gp.split("/")]
+                    cache.set_planner(512, div, (p1, p2, p3))
                 cache.set_sched(int(sv))
             try:
                 cache.alloc(seqs, [0] * B)
