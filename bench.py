@@ -578,7 +578,8 @@ def run_apex(args):
 
     # ---- time prediction (a8) and its online recalibration (f2) at this operating point
     try:
-        result["cost_model"] = cost_model_check(w, wl, ctx_mean_timed, avg_launch_us, hq, hkv)
+        per_step = [float(np.mean(launch_us[k * L:(k + 1) * L])) for k in range(K)]
+        result["cost_model"] = cost_model_check(w, wl, ctx_mean_timed, per_step, hq, hkv)
     except Exception as e:  # the table is a committed profile; its absence is reported, not fatal
         result["cost_model"] = {"error": str(e)}
 
@@ -757,26 +758,34 @@ def run_e2e(args, cache, inputs, seq, B, hq, hkv, D, L, P, tdt, dev, hg, fused_a
                        "-> D2H of out ") + "on a D2H stream -> pinned host"}
 
 
-def cost_model_check(w, wl, ctx_mean, measured_us, hq, hkv):
+def cost_model_check(w, wl, ctx_mean, step_call_us, hq, hkv):
     """a8 + f2 at the benched operating point: predict the layer-call time from the
     committed calibrated table (profiles/cost_table_b200.json, built for full-head
-    LLaMA-3.1-8B GQA calls), then feed the measured time to apex_cost_observe and
-    predict again (online recalibration)."""
+    LLaMA-3.1-8B GQA calls), then feed the measured mean call time of every timed step
+    to apex_cost_observe (alpha 0.5: online recalibration) and report
+    the prediction after each observation's update."""
     from paper_2506_03296_b200 import apex as A
     with open(os.path.join(ROOT, "profiles", "cost_table_b200.json")) as f:
         tab = json.load(f)
     if (w.num_q_heads, w.num_kv_heads, w.dtype) != (32, 8, "bf16") or (hq, hkv) != (32, 8):
         return {"skipped": "the calibrated table covers full-head LLaMA-3.1-8B GQA bf16 calls only"}
     batch, kv_tokens = len(wl["ctx"]), int(round(ctx_mean * len(wl["ctx"])))
+    measured = float(np.mean(step_call_us))
     h = A.apex_cost_create(tab["batch"], tab["kv_tokens"], tab["us"])
     try:
         pred = A.apex_predict_time(h, batch, kv_tokens)
-        out = {"batch": batch, "kv_tokens": kv_tokens, "predicted_us": pred, "measured_us": measured_us,
-               "rel_err": (pred - measured_us) / measured_us}
-        if hasattr(A, "apex_cost_observe"):
-            A.apex_cost_observe(h, batch, kv_tokens, measured_us, 0.5)
-            out["predicted_us_after_observe"] = A.apex_predict_time(h, batch, kv_tokens)
-        return out
+        trace = []
+        for us in step_call_us:
+            A.apex_cost_observe(h, batch, kv_tokens, float(us), 0.5)
+            trace.append(A.apex_predict_time(h, batch, kv_tokens))
+        bg, kg, _ = A.apex_cost_table(h)
+        return {"batch": batch, "kv_tokens": kv_tokens, "table_grid": [[min(tab["batch"]), max(tab["batch"])],
+                                                                       [min(tab["kv_tokens"]), max(tab["kv_tokens"])]],
+                "predicted_us": pred, "measured_us": measured, "rel_err": (pred - measured) / measured,
+                "observations": len(step_call_us), "alpha": 0.5,
+                "predicted_us_after_observe": trace[-1] if trace else pred,
+                "rel_err_after_observe": ((trace[-1] if trace else pred) - measured) / measured,
+                "grid_after_observe": [len(bg), len(kg)]}
     finally:
         A.apex_cost_destroy(h)
 

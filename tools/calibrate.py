@@ -23,8 +23,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-BATCH = [1, 4, 16, 64, 256]
-KV_TOTAL = [1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22]
+# covers the benched operating points: C3 (128, 1M), C4 (256, 4.5M), C5 (1024, 16.8M)
+BATCH = [1, 4, 16, 64, 256, 1024]
+KV_TOTAL = [1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24]
 
 
 def measure(dtype, hq, hkv, batch, total, reps, flush):
@@ -35,7 +36,8 @@ def measure(dtype, hq, hkv, batch, total, reps, flush):
     cache = make_cache(dtype, hq, hkv, batch * (-(-(ctx + 1) // 16)) + 8, max_seqs=batch,
                        max_blocks_per_seq=-(-(ctx + 1) // 16) + 1, max_new_tokens=1 << 22)
     seqs = list(range(batch))
-    prefill(cache, seqs, [ctx] * batch)
+    # very long single contexts are grown 1M tokens at a time (bounded append size)
+    prefill(cache, seqs, [ctx] * batch, interleave=(1 << 20) if ctx > (1 << 21) else 0)
     cache.alloc(seqs, [1] * batch)
     k = gen_dev(cache, 1, 0, seqs, [ctx - 1] * batch, hkv)
     cache.append(0, k, k)
@@ -83,7 +85,7 @@ def main():
     held = []
     for _ in range(a.heldout):
         b = rnd.randint(BATCH[0], BATCH[-1])
-        t = int(2 ** rnd.uniform(14, 22))
+        t = int(2 ** rnd.uniform(14, 24))
         t = max(t, b * 16)
         m, t_real = measure(a.dtype, a.hq, a.hkv, b, t, a.reps, flush)
         p = A.apex_predict_time(h, b, t_real)

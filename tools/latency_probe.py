@@ -27,6 +27,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--shape", default="", help="dtype,hq,hkv,batch,ctx (default: the built-in list)")
+    ap.add_argument("--sched", type=int, default=None, help="apex_kv_set_sched value")
+    ap.add_argument("--lat-tiles", type=int, default=512, help="apex_kv_set_planner latency_tiles_per_cta")
+    ap.add_argument("--graph", action="store_true", help="time a CUDA-graph replay of the call")
+    ap.add_argument("--sched", type=int, default=None, help="apex_kv_set_sched value")
+    ap.add_argument("--lat-tiles", type=int, default=512, help="apex_kv_set_planner latency_tiles_per_cta")
+    ap.add_argument("--graph", action="store_true", help="time a CUDA-graph replay of the call")
     a = ap.parse_args()
     shapes = SHAPES
     if a.shape:
@@ -38,17 +44,30 @@ def main():
                            max_blocks_per_seq=-(-(ctx + 1) // 16) + 1, max_new_tokens=1 << 22)
         seqs = list(range(batch))
         prefill(cache, seqs, [ctx] * batch)
+        cache.set_planner(a.lat_tiles)
+        if a.sched is not None:
+            cache.set_sched(a.sched)
         cache.alloc(seqs, [1] * batch)
         k = gen_dev(cache, 1, 0, seqs, [ctx] * batch, hkv)
         cache.append(0, k, k)
         q = gen_dev(cache, 0, 0, seqs, [ctx] * batch, hq)
         out = torch.empty_like(q)
         times = []
+        graph = None
+        if a.graph:
+            cache.decode(0, q, out=out)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cache.decode(0, q, out=out)
         for r in range(a.reps + 3):
             flush.fill_(r & 0xff)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            cache.decode(0, q, out=out)
+            if graph is not None:
+                graph.replay()
+            else:
+                cache.decode(0, q, out=out)
             e1.record()
             torch.cuda.synchronize()
             if r >= 3:
@@ -58,7 +77,8 @@ def main():
         us = statistics.median(times)
         print(json.dumps({"dtype": dtype, "hq": hq, "hkv": hkv, "batch": batch, "ctx": ctx + 1, "us": round(us, 2),
                           "us_min": round(min(times), 2), "items": len(cache.plan()[0]),
-                          "launches": cache.decode_launches(), "gbs": round(kv / us / 1e3, 1)}), flush=True)
+                          "launches": cache.decode_launches(), "gbs": round(kv / us / 1e3, 1),
+                          "sched": a.sched, "lat_tiles": a.lat_tiles, "graph": a.graph}), flush=True)
         cache.close()
         del cache
         torch.cuda.empty_cache()
