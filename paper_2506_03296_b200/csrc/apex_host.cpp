@@ -311,6 +311,8 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
             }
         }
         cudaError_t e = apex::decode_prepare(desc->dtype, kv->group);
+        if (e == cudaSuccess) e = apex::append_prepare();
+        if (e == cudaSuccess) e = apex::signal_prepare();
         if (e != cudaSuccess) {
             apex_kv_destroy(kv);
             return cuda_fail(e, "apex_kv_create: decode kernel attributes");

@@ -126,7 +126,11 @@ cudaError_t launch_signal_post(uint32_t *const *dst, int n_dst, int slot, uint32
 // persistent-grid size the decode kernel of (dtype, group) runs with on this device
 int decode_grid_ctas(apex_dtype dt, int group, int sm_count);
 bool decode_supported(apex_dtype dt, int group);
-// bytes of dynamic shared memory the decode kernel needs (for attribute setup)
+// attribute setup + eager loading of every kernel a handle may launch (CUDA lazy
+// loading would load a kernel at its first launch, which can block behind a spinning
+// apex_signal_wait kernel and deadlock until its timeout)
 cudaError_t decode_prepare(apex_dtype dt, int group);
+cudaError_t append_prepare();
+cudaError_t signal_prepare();
 
 }  // namespace apex

@@ -71,4 +71,13 @@ cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, v
     return cudaGetLastError();
 }
 
+// Load the kernels now (CUDA lazy loading would otherwise load them at their first
+// launch, which can block behind a spinning kernel such as apex_signal_wait's).
+cudaError_t append_prepare() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, apex_append_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, apex_apply_deltas_kernel);
+    return e;
+}
+
 }  // namespace apex

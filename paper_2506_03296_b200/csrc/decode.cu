@@ -960,7 +960,9 @@ template <int DT, int G> cudaError_t prepare() {
         cudaError_t e = cudaFuncSetAttribute(k[i], cudaFuncAttributeMaxDynamicSharedMemorySize, sm[i]);
         if (e != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    // load the merge kernel now as well (see append_prepare)
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, apex_merge_kernel<DT, G>);
 }
 
 // Decode and merge kernels are launched with programmatic dependent launch:

@@ -63,4 +63,11 @@ cudaError_t launch_signal_post(uint32_t *const *dst, int n_dst, int slot, uint32
     return cudaPeekAtLastError();
 }
 
+cudaError_t signal_prepare() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, apex_signal_wait_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, apex_signal_post_kernel);
+    return e;
+}
+
 }  // namespace apex

@@ -46,3 +46,31 @@ def test_full_block_table_row(cuda_lib, dtype, hq, hkv):
     torch.cuda.synchronize()
     assert cache.seq_info(0)[0] == mbps * 16
     check_close(to_f64(out, dtype), oracle_rows(seqs, ctx, hq, hkv, dtype), dtype)
+
+
+@pytest.mark.gpu
+def test_failed_alloc_leaves_device_state_usable(cuda_lib):
+    """a planner-capacity failure (forced 16-token split over a huge
+    step) and a block-exhaustion failure change nothing -- host mirror, device block
+    table and lengths stay consistent, so the next step decodes correctly (oracle)."""
+    import torch
+
+    from helpers import check_close, decode_step, make_cache, oracle_rows, prefill, to_f64
+    ctx = [40, 300, 17]
+    seqs = [0, 1, 2]
+    cache = make_cache("bf16", 32, 8, num_blocks=6000, max_seqs=8, max_blocks_per_seq=1500, max_batch=8,
+                       max_new_tokens=1 << 17)
+    prefill(cache, seqs, ctx)
+    before = (cache.num_free_blocks(), [cache.seq_info(s) for s in seqs])
+    cache.set_split(16)
+    with pytest.raises(A.ApexError) as e:        # 5000 blocks fit the pool, but 40000 one-block items
+        cache.alloc([3, 4, 5, 6], [20000] * 4)   # exceed the work-list capacity: the planner fails
+    assert e.value.code == "EINVAL" and "work items" in str(e.value)
+    with pytest.raises(A.ApexError) as e:        # more blocks than the pool has left
+        cache.alloc([3, 4, 5, 6, 7], [23000] * 5)
+    assert e.value.code == "ENOBLOCKS"
+    assert (cache.num_free_blocks(), [cache.seq_info(s) for s in seqs]) == before
+    cache.set_split(0)
+    out = decode_step(cache, seqs, ctx)
+    torch.cuda.synchronize()
+    check_close(to_f64(out, "bf16"), oracle_rows(seqs, ctx, 32, 8, "bf16"), "bf16")

@@ -30,15 +30,16 @@ def main():
     ap.add_argument("--sched", type=int, default=None, help="apex_kv_set_sched value")
     ap.add_argument("--lat-tiles", type=int, default=512, help="apex_kv_set_planner latency_tiles_per_cta")
     ap.add_argument("--graph", action="store_true", help="time a CUDA-graph replay of the call")
-    ap.add_argument("--sched", type=int, default=None, help="apex_kv_set_sched value")
-    ap.add_argument("--lat-tiles", type=int, default=512, help="apex_kv_set_planner latency_tiles_per_cta")
-    ap.add_argument("--graph", action="store_true", help="time a CUDA-graph replay of the call")
+    ap.add_argument("--flush", choices=["read", "write"], default="read",
+                    help="L2 flush before each call: read a 512 MiB buffer (L2 left clean) or write it (L2 left "
+                         "full of dirty lines whose write-back competes with the decode's reads)")
     a = ap.parse_args()
     shapes = SHAPES
     if a.shape:
         d, *n = a.shape.split(",")
         shapes = [(d, *[int(x) for x in n])]
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.zeros(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_sink = torch.zeros((), dtype=torch.int64, device="cuda")
     for dtype, hq, hkv, batch, ctx in shapes:
         cache = make_cache(dtype, hq, hkv, batch * (-(-(ctx + 1) // 16)) + 8, max_seqs=batch,
                            max_blocks_per_seq=-(-(ctx + 1) // 16) + 1, max_new_tokens=1 << 22)
@@ -61,7 +62,10 @@ def main():
             with torch.cuda.graph(graph):
                 cache.decode(0, q, out=out)
         for r in range(a.reps + 3):
-            flush.fill_(r & 0xff)
+            if a.flush == "write":
+                flush.fill_(r & 0xff)
+            else:
+                flush_sink.copy_(flush.view(torch.int64).sum())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             if graph is not None:
@@ -78,7 +82,8 @@ def main():
         print(json.dumps({"dtype": dtype, "hq": hq, "hkv": hkv, "batch": batch, "ctx": ctx + 1, "us": round(us, 2),
                           "us_min": round(min(times), 2), "items": len(cache.plan()[0]),
                           "launches": cache.decode_launches(), "gbs": round(kv / us / 1e3, 1),
-                          "sched": a.sched, "lat_tiles": a.lat_tiles, "graph": a.graph}), flush=True)
+                          "sched": a.sched, "lat_tiles": a.lat_tiles, "graph": a.graph,
+                          "flush": a.flush}), flush=True)
         cache.close()
         del cache
         torch.cuda.empty_cache()
