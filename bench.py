@@ -350,6 +350,11 @@ def run_apex(args):
         else:
             dist.init_process_group("nccl", device_id=dev)
     coll_dev = torch.device("cpu") if gloo else dev   # where small reduction tensors live
+
+    def min_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
     w = WORKLOADS[args.config]
     mode = resolve_mode(w, world, args.mode)
     wl = rank_workload(w, rank, world, mode)
@@ -368,11 +373,18 @@ def run_apex(args):
     blocks_per_layer = int(sum(-(-(int(c) + n_steps_total) // 16) for c in ctx0)) + 16
     layer_bytes = blocks_per_layer * hkv * 16 * D * es * 2
     free, _ = torch.cuda.mem_get_info(dev)
+    if world > 1:
+        # every rank must map logical layers onto the same number of pools (the head
+        # slices of one layer are gathered together); with ranks sharing a GPU, a rank
+        # that queries after another allocated would otherwise pick a smaller P
+        free = int(min_over_ranks(float(free)))
     if shared:
         free //= world                                # the ranks split one GPU's memory
     chunk_rows = 1 << 19
     reserve = 6 * 2 ** 30 + 4 * chunk_rows * max(hkv, 1) * D * es
     P = args.phys_layers or max(1, min(L, int((free - reserve) * 0.95) // layer_bytes))
+    if world > 1:
+        P = int(min_over_ranks(float(P)))
     cache = PagedKVCache(num_layers=P, num_q_heads=hq, num_kv_heads=hkv, num_blocks=blocks_per_layer,
                          max_seqs=B, max_blocks_per_seq=mbps, max_batch=B,
                          max_new_tokens=max(chunk_rows, B) + int(ctx0.max()), dtype=dt, device=dev)
@@ -600,9 +612,11 @@ def run_apex(args):
         got = outs[p_last].to(torch.float64).cpu().numpy()
         errs = [float(np.abs(got[i] - o_ref[i]).max()) for i in o_ref]
         rel = [float((np.abs(got[i] - o_ref[i]).max(axis=-1) / np.abs(o_ref[i]).max(axis=-1)).max()) for i in o_ref]
+        ok = max(rel) <= 1e-5 if dt == "f32" else max(errs) <= 2e-2
         result["parity_sample"] = {"requests": sorted(int(i) for i in o_ref), "rows": len(o_ref) * hq,
                                    "max_abs_err": max(errs), "max_row_normwise_err": max(rel),
-                                   "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)"}
+                                   "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)",
+                                   "within_tolerance": bool(ok)}
         # single-thread oracle on the same requests (bounded), for the per-core rate
         rate1, t1s, _, kv_tok1 = sampler.run(ctx_now, min(4.0, args.cpu_seconds / 2), max_requests=1, nthreads=1)
         full_rows = float((ctx_now * hq).sum()) * L
@@ -636,10 +650,14 @@ def run_apex(args):
             got_t = outs[p_last]
         got = got_t.to(torch.float64).cpu().numpy()
         errs = [float(np.abs(got[i] - o_ref[i]).max()) for i in o_ref]
+        rel = [float((np.abs(got[i] - o_ref[i]).max(axis=-1) / np.abs(o_ref[i]).max(axis=-1)).max()) for i in o_ref]
+        ok = max(rel) <= 1e-5 if dt == "f32" else max(errs) <= 2e-2
         result["parity_sample"] = {"requests": sorted(int(wl["ids"][i]) for i in o_ref),
                                    "rows": len(o_ref) * w.num_q_heads, "max_abs_err": max(errs),
+                                   "max_row_normwise_err": max(rel),
                                    "checked": "all-gathered heads" if head_mode else "rank-0 requests",
-                                   "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)"}
+                                   "tolerance": "2e-2 abs (16-bit) / 1e-5 row-normwise (fp32)",
+                                   "within_tolerance": bool(ok)}
     # ---- end-to-end leg: host (pinned) inputs -> C ABI -> host outputs, every step
     if not args.no_e2e:
         e2e = run_e2e(args, cache, inputs, seq, B, hq, hkv, D, L, P, tdt, dev, hg, fused_append,

@@ -314,3 +314,29 @@ def test_continuous_batching_churn(cuda_lib):
         ctx = [live[s] for s in seqs]
         ref = oracle_rows(b_ids, ctx, hq, hkv, dtype)
         check_close(to_f64(out, dtype), ref, dtype)
+
+
+@pytest.mark.parametrize("dtype,hq,hkv,ctx", [("bf16", 32, 8, [16384]),          # 8 pairs x 37 parts
+                                              ("f16", 32, 32, [4096]),           # 32 pairs x 9 parts (8 + 1)
+                                              ("bf16", 16, 2, [20000, 3]),       # uneven parts per pair
+                                              ("f32", 8, 8, [6000])])
+def test_latency_regime_two_level_merge(cuda_lib, dtype, hq, hkv, ctx):
+    """Fused (latency-regime) merge of pairs split into more than kMergeGroup = 8 parts:
+    groups of 8 merged by their last arriver into the group's first slot, then the groups
+    merged by the last group (decode.cu).  Checked against the oracle, over two calls
+    (counters re-armed), with the plan asserted to exercise the two-level path."""
+    import torch
+    cache, seqs, out = run_case(dtype, hq, hkv, ctx)
+    items, n_merges = cache.plan()
+    assert cache.decode_launches() == 1
+    parts = {}
+    for (b, g, blk0, nblk, part, seq) in items:
+        if part >= 0:
+            parts[(b, g)] = parts.get((b, g), 0) + 1
+    assert parts and max(parts.values()) > 8, parts
+    ref = oracle_rows(seqs, ctx, hq, hkv, dtype)
+    check_close(out, ref, dtype)
+    q = gen_dev(cache, 0, 0, seqs, [c - 1 for c in ctx], hq)
+    again = cache.decode(0, q)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_f64(again, dtype), out)          # deterministic, counters re-armed
