@@ -86,8 +86,7 @@ int query_sm_count(bool host_only) {
 // merges, slots, block-table deltas, length deltas) into `upload`.
 struct WsLayout {
     int32_t max_items = 0, max_merges = 0, max_bt_delta = 0;
-    size_t counters = 0, merge_counters = 0, part_counters = 0, upload = 0, upload_cap = 0, part_o = 0,
-           part_ml = 0, group_ml = 0, total = 0;
+    size_t counters = 0, merge_counters = 0, upload = 0, upload_cap = 0, part_o = 0, part_ml = 0, total = 0;
     size_t o_items = 0, o_merges = 0, o_tail = 0;             // offsets inside the upload region
 };
 
@@ -112,14 +111,11 @@ WsLayout layout_for(const apex_kv_desc *d, int sm_count) {
     up += align_up(sizeof(int2) * (size_t)d->max_batch, 256);
     w.counters = 0;                                           // 3 counters x 64 layers (queue, done, signal)
     w.merge_counters = 1024;                                  // one per split pair
-    // one per partial slot: arrivals of a merge group, counted at the group's first slot
-    w.part_counters = align_up(w.merge_counters + sizeof(int32_t) * (size_t)w.max_merges, 256);
-    w.upload = align_up(w.part_counters + sizeof(int32_t) * (size_t)w.max_items, 256);
+    w.upload = align_up(w.merge_counters + sizeof(int32_t) * (size_t)w.max_merges, 256);
     w.upload_cap = up;
     w.part_o = align_up(w.upload + up, 256);
     w.part_ml = align_up(w.part_o + sizeof(float) * (size_t)w.max_items * G * d->head_dim, 256);
-    w.group_ml = align_up(w.part_ml + sizeof(float) * 2 * (size_t)w.max_items * G, 256);
-    w.total = align_up(w.group_ml + sizeof(float) * 2 * (size_t)w.max_items * G, 256);
+    w.total = align_up(w.part_ml + sizeof(float) * 2 * (size_t)w.max_items * G, 256);
     return w;
 }
 
@@ -882,8 +878,6 @@ static apex_status decode_impl(apex_kv *kv, int32_t layer, const void *q, const 
     p.counters = (int32_t *)(ws + kv->ws.counters) + 2 * layer;
     p.sig_counter = (int32_t *)(ws + kv->ws.counters) + 2 * apex::kMaxLayers + layer;
     p.merge_counters = (int32_t *)(ws + kv->ws.merge_counters);
-    p.part_counters = (int32_t *)(ws + kv->ws.part_counters);
-    p.group_ml = (float *)(ws + kv->ws.group_ml);
     p.merge_grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kv->ws.max_merges, 16LL * kv->sm_count));
     p.max_blocks_per_seq = kv->d.max_blocks_per_seq;
     p.num_q_heads = kv->d.num_q_heads;

@@ -14,7 +14,6 @@ constexpr int kBlock = 16;          // tokens per KV block (reading c9)
 constexpr int kHeadDim = 128;       // D
 constexpr int kMaxLayers = 64;
 constexpr int kMaxOut = 8;          // destinations of apex_decode_attention_ex
-constexpr int kMergeGroup = 8;      // fused (latency-regime) merge: parts merged per first-level group
 
 // One split-KV work item: the tokens of logical blocks [blk0, blk0+nblk) of
 // (batch row b, kv head g).  32 bytes, read once per item by the decode kernel.
@@ -83,9 +82,7 @@ struct DecodeParams {
     float *part_o;             // [slots][G][D]   unnormalised sum_t p_t v_t (fp32)
     float *part_ml;            // [slots][G][2]   (running max m in log2 units, sum l)
     int32_t *counters;         // [2]: work-queue head, CTAs done
-    int32_t *merge_counters;   // [n_merges]: split items (or merge groups) finished per pair (left at 0)
-    int32_t *part_counters;    // [slots]: split items finished per merge group, at the group's first slot
-    float *group_ml;           // [slots][G][2]: (m, l) of a merge group's partial, at its first slot
+    int32_t *merge_counters;   // [n_merges]: split items finished per pair (left at 0)
     const StepHeader *hdr;     // this step's counts (device, written by apex_kv_alloc's upload)
     const int32_t *cta_begin;  // [grid + 1] static item ranges, then the dynamic queue base
     int32_t merge_grid;        // fixed grid of the merge kernel (grid-stride over hdr->n_merges)

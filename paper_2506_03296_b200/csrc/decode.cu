@@ -616,47 +616,34 @@ template <int DT, bool FUSE> struct ConsumerSel<DT, 1, FUSE> {
     using T = typename std::conditional<DT != APEX_F32 && FUSE, MmaConsumerT<DT, 1>, SimtConsumer<DT>>::type;
 };
 
-// log-sum-exp merge of split partials, combined in split order:
+// log-sum-exp merge of one split (b, g) pair, partials combined in split order:
 // M = max m_i, out = sum 2^(m_i-M) O_i / sum 2^(m_i-M) l_i.  Partials written by
 // other CTAs are read through L2 (ld.global.cg).
-//
-// Sources: parts i < np at slot part0 + i*stride, O from part_o, (m, l) from ml_src
-// (part_ml, or group_ml for first-level group results).  Destination: dst_slot < 0
-// -> the final output rows (store_out); else the unnormalised merged O goes to
-// part_o slot dst_slot (the group's first slot: every thread reads its own O
-// elements before writing them, so in place is safe) and (M, den) to group_ml.
 //
 // One pass with a running max: thread (output float4 o, part group gr) folds
 // parts i = gr, gr + ngr, ... into (M, den, acc) with acc <- acc 2^(M-M') +
 // 2^(m_i-M') O_i.  The loads of all parts are independent of the running state,
-// so an unrolled loop keeps 16 parts in flight per thread.  Part groups (ngr > 1)
-// are combined through `red`/`redml` in fixed group order.  `sync` is a barrier
-// over the nt participating threads.
+// so an unrolled loop keeps 16 parts in flight per thread (a 37-way merge is
+// ~3 round trips; the former max-then-sum form needed a dependent second pass).
+// Part groups (ngr > 1, separate merge kernel: 256 threads) are combined
+// through `red`/`redml` in fixed group order.  `sync` is a barrier over the nt
+// participating threads.
 template <int DT, int G, typename Sync>
-__device__ __forceinline__ void merge_parts(const DecodeParams &p, int mb, int mgk, int part0, int np, int stride,
-                                            const float *ml_src, int dst_slot, int t, int nt, float4 *red,
-                                            float2 *redml, int red_cap, Sync sync) {
+__device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt, float4 *red,
+                                           float2 *redml, int red_cap, Sync sync) {
+    const int np = mg.nparts;
     constexpr int NOUT = G * kHeadDim / 4;                    // float4 outputs of the pair
-    const float2 *ml = reinterpret_cast<const float2 *>(ml_src) + (size_t)part0 * G;
-    const size_t pstride = (size_t)stride * G;               // float2 / D-vector slots between parts
+    const float2 *ml = reinterpret_cast<const float2 *>(p.part_ml) + (size_t)mg.part0 * G;
     const int ngr = red ? max(1, min(nt, red_cap) / NOUT) : 1;   // part groups (1 when NOUT >= nt)
-    auto emit = [&](int row, int d4, float M, float den, float a, float b, float c, float d) {
-        if (dst_slot < 0) {
-            store_out<DT>(p, mb, mgk * G + row, d4, a / den, b / den, c / den, d / den);
-        } else {
-            *reinterpret_cast<float4 *>(p.part_o + ((size_t)dst_slot * G + row) * kHeadDim + d4) = make_float4(a, b, c, d);
-            if (d4 == 0) *reinterpret_cast<float2 *>(p.group_ml + ((size_t)dst_slot * G + row) * 2) = make_float2(M, den);
-        }
-    };
     for (int idx = t; idx < NOUT * ngr; idx += nt) {
         const int o = idx % NOUT, gr = idx / NOUT;
         const int row = o / (kHeadDim / 4), d4 = (o % (kHeadDim / 4)) * 4;
-        const float *po = p.part_o + ((size_t)part0 * G + row) * kHeadDim + d4;
+        const float *po = p.part_o + ((size_t)mg.part0 * G + row) * kHeadDim + d4;
         float M = -INFINITY, den = 0.f, a = 0.f, b = 0.f, c = 0.f, d = 0.f;
 #pragma unroll kMergeUnroll
         for (int i = gr; i < np; i += ngr) {
-            const float2 mi = __ldcg(ml + (size_t)i * pstride + row);
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + (size_t)i * pstride * kHeadDim));
+            const float2 mi = __ldcg(ml + (size_t)i * G + row);
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + (size_t)i * G * kHeadDim));
             const float Mn = fmaxf(M, mi.x);
             const float al = ex2_diff(M, Mn), e = ex2_diff(mi.x, Mn);
             den = fmaf(den, al, e * mi.y);
@@ -667,7 +654,7 @@ __device__ __forceinline__ void merge_parts(const DecodeParams &p, int mb, int m
             M = Mn;
         }
         if (ngr == 1) {
-            emit(row, d4, M, den, a, b, c, d);
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
         } else {
             red[gr * NOUT + o] = make_float4(a, b, c, d);
             redml[gr * NOUT + o] = make_float2(M, den);
@@ -690,7 +677,7 @@ __device__ __forceinline__ void merge_parts(const DecodeParams &p, int mb, int m
                 c = fmaf(e, v.z, c);
                 d = fmaf(e, v.w, d);
             }
-            emit(row, d4, M, den, a, b, c, d);
+            store_out<DT>(p, mg.b, mg.g * G + row, d4, a / den, b / den, c / den, d / den);
         }
         sync();                                                // red reusable for the next pair
     }
@@ -898,74 +885,35 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             if (k == 0 && threadIdx.x == 32) TRACE(8);
 #endif
             if (FUSE && it.part >= 0) {
-                // the last-arriving split of this (b, g) pair merges the partials (fused LSE
+                // last-arriving split of this (b, g) pair merges all its partials (fused LSE
                 // merge).  Release/acquire through one thread (CUTLASS-semaphore pattern):
                 // bar.sync orders the CTA's partial stores before thread 32's gpu-scope
                 // acq_rel fence + counter atomic; the last arriver's fence + bar.sync order
                 // the other CTAs' partials before every thread's loads (no per-thread
-                // sequentially consistent __threadfence).  Pairs split into more than
-                // kMergeGroup parts merge in two levels: the last arriver of each group of
-                // kMergeGroup parts merges the group into the group's first slot, and the
-                // last group to finish merges the groups -- two short rounds of L2 loads
-                // instead of one long chain (batch-1 long contexts split 37 ways).
-                const MergeItem mgi = merges_of(p)[it.mg];
-                const int np = mgi.nparts;
-                const bool two_level = np > kMergeGroup;
-                const int gk = (it.part - mgi.part0) / kMergeGroup;
-                const int gfirst = mgi.part0 + gk * kMergeGroup;
-                const int gsize = min(kMergeGroup, np - gk * kMergeGroup);
+                // sequentially consistent __threadfence).
                 named_bar_sync(1, NC * 32);
                 if (threadIdx.x == 32) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    int flag = 0;
-                    if (!two_level) {
-                        if (atomicAdd(p.merge_counters + it.mg, 1) == np - 1) {
-                            p.merge_counters[it.mg] = 0;        // every split has arrived: re-arm
-                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                            flag = 1;
-                        }
-                    } else if (atomicAdd(p.part_counters + gfirst, 1) == gsize - 1) {
-                        p.part_counters[gfirst] = 0;
+                    const int done = atomicAdd(p.merge_counters + it.mg, 1);
+                    const int last = done == merges_of(p)[it.mg].nparts - 1;
+                    if (last) {
+                        p.merge_counters[it.mg] = 0;            // every split has arrived: re-arm
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                        flag = 2;
                     }
-                    *merge_flag = flag;
+                    *merge_flag = last;
                 }
                 named_bar_sync(1, NC * 32);
 #ifdef APEX_TRACE
                 if (k == 0 && threadIdx.x == 32) TRACE(9);
 #endif
-                const int flag = *merge_flag;
-                if (flag == 1) {
-                    merge_parts<DT, G>(p, mgi.b, mgi.g, mgi.part0, np, 1, p.part_ml, -1, threadIdx.x - 32, NC * 32,
-                                       mred, mredml, NC * 32, [] { named_bar_sync(1, NC * 32); });
-                } else if (flag == 2) {
-                    merge_parts<DT, G>(p, mgi.b, mgi.g, gfirst, gsize, 1, p.part_ml, gfirst, threadIdx.x - 32,
-                                       NC * 32, mred, mredml, NC * 32, [] { named_bar_sync(1, NC * 32); });
-                    named_bar_sync(1, NC * 32);                 // group result stored by every thread
-                    if (threadIdx.x == 32) {
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                        const int ngroups = (np + kMergeGroup - 1) / kMergeGroup;
-                        int last = 0;
-                        if (atomicAdd(p.merge_counters + it.mg, 1) == ngroups - 1) {
-                            p.merge_counters[it.mg] = 0;
-                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                            last = 1;
-                        }
-                        *merge_flag = last;
-                    }
-                    named_bar_sync(1, NC * 32);
-                    if (*merge_flag)
-                        merge_parts<DT, G>(p, mgi.b, mgi.g, mgi.part0, (np + kMergeGroup - 1) / kMergeGroup,
-                                           kMergeGroup, p.group_ml, -1, threadIdx.x - 32, NC * 32, mred, mredml,
-                                           NC * 32, [] { named_bar_sync(1, NC * 32); });
-                }
+                if (*merge_flag) {
+                    merge_pair<DT, G>(p, merges_of(p)[it.mg], threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
+                                      [] { named_bar_sync(1, NC * 32); });
 #ifdef APEX_TRACE
-                if (flag) {
                     named_bar_sync(1, NC * 32);
                     if (threadIdx.x == 32) TRACE(10);
-                }
 #endif
+                }
             }
             named_bar_sync(1, NC * 32);
         }
@@ -994,11 +942,9 @@ __global__ void __launch_bounds__(kMergeThreads) apex_merge_kernel(const DecodeP
     __shared__ float2 redml[kMergeThreads];
     asm volatile("griddepcontrol.wait;" ::: "memory");     // partials of the decode kernel
     const int n = p.hdr->n_merges;                          // fixed grid, grid-stride over this step's pairs
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const MergeItem mg = merges_of(p)[i];
-        merge_parts<DT, G>(p, mg.b, mg.g, mg.part0, mg.nparts, 1, p.part_ml, -1, threadIdx.x, blockDim.x, red, redml,
-                           kMergeThreads, [] { __syncthreads(); });
-    }
+    for (int i = blockIdx.x; i < n; i += gridDim.x)
+        merge_pair<DT, G>(p, merges_of(p)[i], threadIdx.x, blockDim.x, red, redml, kMergeThreads,
+                          [] { __syncthreads(); });
     signal_done(p);   // runs after the decode grid completed (griddepcontrol.wait): all rows stored
 }
 

@@ -320,11 +320,12 @@ def test_continuous_batching_churn(cuda_lib):
                                               ("f16", 32, 32, [4096]),           # 32 pairs x 9 parts (8 + 1)
                                               ("bf16", 16, 2, [20000, 3]),       # uneven parts per pair
                                               ("f32", 8, 8, [6000])])
-def test_latency_regime_two_level_merge(cuda_lib, dtype, hq, hkv, ctx):
-    """Fused (latency-regime) merge of pairs split into more than kMergeGroup = 8 parts:
-    groups of 8 merged by their last arriver into the group's first slot, then the groups
-    merged by the last group (decode.cu).  Checked against the oracle, over two calls
-    (counters re-armed), with the plan asserted to exercise the two-level path."""
+def test_latency_regime_many_part_merge(cuda_lib, dtype, hq, hkv, ctx):
+    """Fused (latency-regime) LSE merge of pairs split into many parts (up to ~150):
+    the last arriving split merges all partials in-kernel.  Checked against the oracle,
+    over two calls (arrival counters re-armed), with the plan asserted to split pairs
+    into more than 8 parts.  (A two-level merge tree for these pairs was measured
+    slower -- DESIGN.md section 8 -- and not kept.)"""
     import torch
     cache, seqs, out = run_case(dtype, hq, hkv, ctx)
     items, n_merges = cache.plan()
