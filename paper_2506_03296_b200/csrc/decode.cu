@@ -51,9 +51,14 @@ __device__ __forceinline__ void trace(int ev) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 1024) g_apex_trace[blockIdx.x][ev] = t;
 }
+__device__ __forceinline__ void trace_val(int ev, unsigned long long v) {
+    if (blockIdx.x < 1024) g_apex_trace[blockIdx.x][ev] = v;
+}
 #define TRACE(ev) trace(ev)
+#define TRACE_VAL(ev, v) trace_val(ev, v)
 #else
 #define TRACE(ev) ((void)0)
+#define TRACE_VAL(ev, v) ((void)0)
 #endif
 namespace {
 
@@ -828,6 +833,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             mbar_wait(ifull0 + 8 * slot, use & 1);
             const WorkItem it = ring[slot].it;
             if (it.nblk == 0) break;
+            // the pair's merge record, loaded now so that the arrival test and the fused merge
+            // at the item's end do not start with a dependent (after an L2 flush: DRAM) load
+            MergeItem mgi{};
+            if (FUSE && it.part >= 0) mgi = merges_of(p)[it.mg];
             st.begin(static_cast<const uint8_t *>(p.q) +
                          ((size_t)it.b * p.num_q_heads + (size_t)it.g * G) * kHeadDim * C::ES, p, lane);
             __syncwarp();
@@ -894,8 +903,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 named_bar_sync(1, NC * 32);
                 if (threadIdx.x == 32) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#ifdef APEX_TRACE
+                    if (k == 0) TRACE(13);
+#endif
                     const int done = atomicAdd(p.merge_counters + it.mg, 1);
-                    const int last = done == merges_of(p)[it.mg].nparts - 1;
+                    const int last = done == mgi.nparts - 1;
                     if (last) {
                         p.merge_counters[it.mg] = 0;            // every split has arrived: re-arm
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -904,10 +916,14 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 }
                 named_bar_sync(1, NC * 32);
 #ifdef APEX_TRACE
-                if (k == 0 && threadIdx.x == 32) TRACE(9);
+                if (k == 0 && threadIdx.x == 32) {
+                    TRACE(9);
+                    TRACE_VAL(14, (unsigned long long)it.mg + 1);
+                    TRACE_VAL(15, (unsigned long long)*merge_flag);
+                }
 #endif
                 if (*merge_flag) {
-                    merge_pair<DT, G>(p, merges_of(p)[it.mg], threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
+                    merge_pair<DT, G>(p, mgi, threadIdx.x - 32, NC * 32, mred, mredml, NC * 32,
                                       [] { named_bar_sync(1, NC * 32); });
 #ifdef APEX_TRACE
                     named_bar_sync(1, NC * 32);
@@ -923,6 +939,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     // the merge kernel signals; this kernel's rows are flushed by its completion.
     if (FUSE) {
         signal_done(p);
+#ifdef APEX_TRACE
+        if (threadIdx.x == 0) TRACE(12);
+#endif
     } else if (p.signals[0] != nullptr) {
         __syncthreads();   // this CTA's (possibly peer-mapped) rows before the merge kernel's signal
         if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
