@@ -75,21 +75,27 @@ int main() {
         printf("ldg_read  grid=%d x 256: best %.1f GB/s\n", sms * occ, best);
         best = 0;
     }
-    constexpr int ST = 12, CH = 8192;
-    cudaFuncSetAttribute(bulk_read<ST, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CH);
-    for (int occ : {2, 4}) {
-        for (int rep = 0; rep < 5; ++rep) {
-            cudaEventRecord(a);
-            bulk_read<ST, CH><<<sms * occ, 32, ST * CH>>>(buf, bytes / CH, sink);
-            cudaEventRecord(b);
-            cudaEventSynchronize(b);
-            float ms;
-            cudaEventElapsedTime(&ms, a, b);
-            if (rep) best = best > bytes / ms / 1e6 ? best : bytes / ms / 1e6;
+    auto bulk = [&](auto kern, int st, int ch) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, st * ch);
+        for (int occ : {2, 4}) {
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(a);
+                kern<<<sms * occ, 32, st * ch>>>(buf, bytes / ch, sink);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep) best = best > bytes / ms / 1e6 ? best : bytes / ms / 1e6;
+            }
+            printf("bulk_read grid=%d, %d x %d KiB ring: best %.1f GB/s\n", sms * occ, st, ch / 1024, best);
+            best = 0;
         }
-        printf("bulk_read grid=%d, 12 x 8 KiB ring: best %.1f GB/s\n", sms * occ, best);
-        best = 0;
-    }
+    };
+    // chunk-size sensitivity at ~96 KiB in flight per CTA
+    bulk(bulk_read<12, 8192>, 12, 8192);
+    bulk(bulk_read<6, 16384>, 6, 16384);
+    bulk(bulk_read<3, 32768>, 3, 32768);
+    bulk(bulk_read<24, 4096>, 24, 4096);
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
