@@ -1,6 +1,6 @@
-"""Copy/summarise gpurun_out/refresh/ (tools/refresh_profiles.sh) into profiles/ (round tag r01).
+"""Copy/summarise gpurun_out/refresh/ (tools/refresh_profiles.sh) into profiles/ (round tag).
 
-    python tools/ingest_refresh.py [--src gpurun_out/refresh] [--tag r01]
+    python tools/ingest_refresh.py [--src gpurun_out/refresh] [--tag r02]
 
 Prints the results table used in DESIGN.md §8.
 """
@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--src", default=os.path.join(ROOT, "gpurun_out", "refresh"))
-    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--tag", default="r02")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     src = a.src
@@ -26,17 +26,20 @@ def main():
         cp(f"bench_{c}.json", f"{a.tag}_{c}_bench.json")
         rep = os.path.join(src, f"prof_{c}.ncu-rep")
         if os.path.exists(rep):
+            # key = bench.py's (config, mode, N) lookup for roofline.traffic (N = 1: request mode)
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), "--tag", f"{a.tag}_{c}",
-                            "--config", c, "--rep", rep], check=True, capture_output=True)
+                            "--config", f"{c}:req:1", "--rep", rep], check=True, capture_output=True)
             shutil.copy(rep, os.path.join(prof, f"{a.tag}_{c}_decode.ncu-rep"))
-    cp("bench_reference_c3.json", f"{a.tag}_c3_reference_bench.json")
-    for name, tag in (("launches_c3_timed.csv", "c3_timed"), ("launches_c3_all.csv", "c3")):
+    cp("bench_reference_c5.json", f"{a.tag}_c5_reference_bench.json")
+    cp("latency_probe.jsonl", f"{a.tag}_latency_probe_final.jsonl")
+    cp("gpus2_head.json", f"{a.tag}_gpus2_head_same_gpu.json")
+    cp("gpus2_req.json", f"{a.tag}_gpus2_req_same_gpu.json")
+    cp("clocks_before.txt", f"{a.tag}_refresh_clocks_before.txt")
+    for name, tag in (("launches_c5_timed.csv", "c5_timed"),):
         f = os.path.join(src, name)
         if os.path.exists(f):
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), "--tag", f"{a.tag}_{tag}",
                             "--config", tag, "--launches", f], check=True, capture_output=True)
-    cp("cost_table_b200.json", "cost_table_b200.json")
-    cp("apex_decision_b200.json", "apex_decision_b200.json")
     cp("hbm_probe.txt", f"{a.tag}_hbm_read_probe.txt")
     cp("pytest_gpu.log", f"{a.tag}_pytest_gpu_full.log")
     cp("smoke.log", f"{a.tag}_smoke.log")
@@ -47,7 +50,7 @@ def main():
             continue
         d = json.load(open(f))
         r, p, cb = d["roofline"], d.get("parity_sample", {}), d.get("cpu_baseline", {})
-        rows.append(f"| {c.upper()} | {d['config']['phys_layers']} | {d['value']:.0f} | {d['ms_per_step']:.3f} | "
+        rows.append(f"| {c.upper()} | {d['details']['phys_layers']} | {d['value']:.0f} | {d['ms_per_step']:.3f} | "
                     f"{r['avg_launch_us']:.1f} | {r['achieved']:.0f} | {r['frac']:.3f} | {r['frac_of_8000_gbs']:.3f} | "
                     f"{d['e2e']['value']:.0f} | {cb.get('value', 0):.3g} ({cb.get('cores', '?')} thr) | "
                     f"{p.get('max_abs_err', 0):.1e} | {d.get('clocks', {}).get('sm_mhz', '?')} |")
