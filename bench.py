@@ -102,6 +102,18 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback 6.65 TB/s from B200_PROFILING.md (MEASURED_PEAKS.json absent)"
 
 
+def read_probe_gbs():
+    """Best read-only HBM rate of the committed TMA bulk-copy probe (tools/hbm_probe.cu,
+    8 KiB chunks -- the decode kernel's tile size), or None."""
+    import glob
+    import re
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_hbm_read_probe.txt")))[-1:]:
+        for m in re.finditer(r"bulk_read grid=\d+, 12 x 8 KiB ring: best ([0-9.]+) GB/s", open(f).read()):
+            best = max(best or 0.0, float(m.group(1)))
+    return best
+
+
 def ncu_traffic(config: str, mode: str, world: int):
     """dram bytes/launch of the decode kernel from the committed ncu --set full summary for
     exactly this (config, sharding mode, N), or None."""
@@ -584,7 +596,8 @@ def run_apex(args):
                                      "pairs are merged in a second launch)",
                            "alg_bytes_per_launch": bytes_per_launch, "avg_launch_us": avg_launch_us,
                            "launches_timed": len(launch_us), "peak_source": peak_src,
-                           "frac_of_8000_gbs": achieved_gbs / 8000.0},
+                           "frac_of_8000_gbs": achieved_gbs / 8000.0,
+                           "frac_of_read_probe": (achieved_gbs / probe) if (probe := read_probe_gbs()) else None},
               # ours only (NCCL's kernels excluded): deltas + L x ([append,] decode[, merge])
               # [+ 2 signal kernels per layer with the fused gather]; the append rides in the
               # decode launch only in the latency regime (decode_launches == 1)
