@@ -628,11 +628,13 @@ template <int DT, bool FUSE> struct ConsumerSel<DT, 1, FUSE> {
 // One pass with a running max: thread (output float4 o, part group gr) folds
 // parts i = gr, gr + ngr, ... into (M, den, acc) with acc <- acc 2^(M-M') +
 // 2^(m_i-M') O_i.  The loads of all parts are independent of the running state,
-// so an unrolled loop keeps 16 parts in flight per thread (a 37-way merge is
-// ~3 round trips; the former max-then-sum form needed a dependent second pass).
-// Part groups (ngr > 1, separate merge kernel: 256 threads) are combined
-// through `red`/`redml` in fixed group order.  `sync` is a barrier over the nt
-// participating threads.
+// so the unrolled loop can keep several parts in flight per thread (inside the
+// decode kernel, at its 168-register cap, ptxas serialises part of them: a 37-way
+// merge there measures 10-20 dependent L2 round trips, ~3.5 us; batched, staged
+// and warp-per-row variants were no faster -- profiles/r02_merge_ab.txt).
+// Part groups (ngr = nt / (G * 32) > 1 when the pair has fewer float4 outputs than
+// the nt = 128 participating threads) are combined through `red`/`redml` in fixed
+// group order.  `sync` is a barrier over the nt participating threads.
 template <int DT, int G, typename Sync>
 __device__ __forceinline__ void merge_pair(const DecodeParams &p, const MergeItem mg, int t, int nt, float4 *red,
                                            float2 *redml, int red_cap, Sync sync) {
