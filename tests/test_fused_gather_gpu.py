@@ -218,8 +218,9 @@ def test_signalled_gather_in_kernel_flags(cuda_lib, split):
     ptr = lambda t, off=0: t.data_ptr() + off
     gathers = [SignalledGather(r, world, [[ptr(b) for b in bufs]], [[ptr(s) for s in sig]],
                                [[ptr(s, 4 * world) for s in sig]]) for r in range(world)]
-    torch.cuda.synchronize()
-    reader = torch.cuda.Stream()
+    [b.clone() for b in bufs]                           # load the copy kernel before anything spins: with
+    torch.cuda.synchronize()                            # lazy loading its first launch would block the host
+    reader = torch.cuda.Stream()                        # behind the reader's spinning wait
     writer = torch.cuda.Stream()
     ref = oracle_rows(seqs, ctx, hq, hkv, dtype)
     for epoch in (1, 2):
