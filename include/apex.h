@@ -91,8 +91,12 @@ size_t apex_kv_workspace_bytes(const apex_kv_desc *desc);
 
 /* Validate the desc, build the LIFO free list (first pop = block 0, reading
    c10), the host mirrors, the pinned staging ring and one TMA descriptor per
-   physical layer.  Launches no kernel.  The pools' contents are not
-   touched (callers may pre-fill them, e.g. with NaN in tests). */
+   physical layer; load every kernel the handle may launch (so no later launch
+   waits on CUDA lazy module loading, e.g. behind a spinning apex_signal_wait);
+   zero the workspace's queue / merge / signal counters (cudaMemset, then a
+   device synchronise: create is not on the hot path and the counters must be
+   zero before any stream uses them).  The pools' contents are not touched
+   (callers may pre-fill them, e.g. with NaN in tests). */
 apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out);
 
 /* Free host state.  The caller must synchronise its streams first. */
