@@ -11,8 +11,9 @@ from helpers import check_close, decode_step, gen_dev, make_cache, oracle_rows, 
 
 pytestmark = pytest.mark.gpu
 
+# (dtype, Hq, Hkv); Hkv = 1 is a rank's slice under 8-way head sharding of LLaMA-3.1-8B (C5, N = 8: Hq 4, Hkv 1)
 COMBOS = [("f32", 4, 4), ("f16", 4, 4), ("f16", 8, 4), ("f16", 8, 2), ("f16", 16, 4), ("f16", 16, 2), ("bf16", 8, 4),
-          ("bf16", 16, 4), ("bf16", 16, 2)]
+          ("bf16", 16, 4), ("bf16", 16, 2), ("bf16", 4, 1), ("bf16", 8, 1), ("f16", 2, 1)]
 RAGGED = [1, 2, 15, 16, 17, 31, 64, 100, 257, 1000, 2049]
 
 

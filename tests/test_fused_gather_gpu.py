@@ -15,7 +15,8 @@ from helpers import check_close, gen_dev, make_cache, oracle_rows, to_f64
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dtype,hq,hkv,world", [("bf16", 32, 8, 2), ("bf16", 32, 8, 4), ("f16", 8, 8, 2)])
+@pytest.mark.parametrize("dtype,hq,hkv,world", [("bf16", 32, 8, 2), ("bf16", 32, 8, 4), ("bf16", 32, 8, 8),
+                                                ("f16", 8, 8, 2)])
 def test_head_sharded_epilogue_gather(cuda_lib, dtype, hq, hkv, world):
     import torch
 
