@@ -139,9 +139,10 @@ apex_status apex_kv_append(apex_kv *kv, int32_t layer, const void *k_new, const 
    (seq, kv-head) pairs -- or, for small steps (latency regime), the merge is
    done inside the decode kernel by the last split to finish (see
    apex_kv_decode_launches).  Results are deterministic and independent of the physical
-   block placement.  Supported: F32/F16 with g == 1 (CUDA cores; F16 on tensor
-   cores in the latency regime), F16/BF16 with g in {2,4,8} (tensor cores,
-   mma.sync with the q-group on the N side); otherwise APEX_EUNSUPPORTED.
+   block placement.  Supported: F32 with g == 1 (CUDA cores), F16 with
+   g == 1 and F16/BF16 with g in {2,4,8} (tensor cores, mma.sync with the
+   q-group on the N side; MHA with one live column); otherwise
+   APEX_EUNSUPPORTED.
    CUDA graphs: every launch parameter is step-invariant within a regime, so a
    captured sequence of calls stays valid while apex_kv_decode_launches() is
    unchanged (the regime switches at T = 512 tiles per CTA). */

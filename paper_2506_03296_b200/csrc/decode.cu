@@ -24,9 +24,9 @@
 //    mma.sync.m16n8k16, the q-group on the N = 8 side (16 HMMA per 16-token
 //    tile), K/V fragments via ldmatrix(.trans) on the swizzled tiles
 //    (conflict-free), P^T re-laid from the S^T accumulators by movmatrix.trans;
-//  * MHA (g == 1) and fp32: CUDA-core FMAs, one lane per token for q.K
-//    (conflict-free thanks to the swizzle), lane-owned dims for P.V (16-bit MHA
-//    uses the tensor-core path in the latency regime).
+//  * fp32 (MHA): CUDA-core FMAs, one lane per token for q.K (conflict-free
+//    thanks to the swizzle), lane-owned dims for P.V; 16-bit MHA uses the
+//    tensor-core path above with one live head column (fewer instructions).
 //  * softmax in the log2 domain (scale*log2e folded into S); split items write
 //    (m, l, unnormalised O) fp32 partials merged in split order -- by a second
 //    small launch (fixed grid, grid-stride over split pairs) in the bandwidth
@@ -612,13 +612,14 @@ template <int DT, int G> struct MmaConsumerT {
 };
 
 template <int DT, int G, bool FUSE> struct ConsumerSel { using T = MmaConsumerT<DT, G>; };
-// MHA (g = 1): fp32 on CUDA cores.  16-bit: CUDA cores in the bandwidth regime,
-// the transposed tensor-core path (one live head column: 16 HMMA per tile instead
-// of ~260 FMA/unpack instructions per lane) in the latency regime, where the
-// per-tile latency matters (fp16 batch 8 x 1K: 43 -> 40 us; bandwidth regime C2:
-// 615 -> 622 us, so not there).
+// MHA (g = 1): fp32 on CUDA cores.  16-bit: the transposed tensor-core path with one
+// live head column (16 HMMA per tile instead of ~260 FMA/unpack instructions per lane):
+// faster per tile in the latency regime (fp16 batch 8 x 1K: 43 -> 40 us) and, by
+// issuing half the instructions, cooler in the bandwidth regime -- C2 sustained over
+// 60 steps under sw_power_cap: 1.51 -> 1.58 GHz, 3,134 -> 3,166 tokens/s (+1.0%,
+// same box, 3 rounds); isolated calls 603.0 -> 601.2 us.
 template <int DT, bool FUSE> struct ConsumerSel<DT, 1, FUSE> {
-    using T = typename std::conditional<DT != APEX_F32 && FUSE, MmaConsumerT<DT, 1>, SimtConsumer<DT>>::type;
+    using T = typename std::conditional<DT != APEX_F32, MmaConsumerT<DT, 1>, SimtConsumer<DT>>::type;
 };
 
 // log-sum-exp merge of one split (b, g) pair, partials combined in split order:
