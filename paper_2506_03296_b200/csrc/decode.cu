@@ -749,9 +749,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // trip earlier than a load that waits for cta_begin (the list has >= grid slots)
         const WorkItem spec = p.items[blockIdx.x].it;
         const int spec_ids = lane < kInlineIds ? p.items[blockIdx.x].ids[lane] : 0;
-        int32_t pc[NC];                       // tiles issued to each consumer warp's sub-ring
+        // each consumer warp's sub-ring as (next slot, completed passes); incremental, so the
+        // per-tile path has no division by SW and no run-time warp index (measured: C5 +1.9%,
+        // C3 +1.2% sustained against m % SW, m / SW with the warp picked at run time)
+        int32_t rs[NC], ru[NC];
 #pragma unroll
-        for (int q = 0; q < NC; ++q) pc[q] = 0;
+        for (int q = 0; q < NC; ++q) rs[q] = ru[q] = 0;
         for (int k = 0;; ++k) {
             int idx;
             if (s_next < s_end) {
@@ -790,28 +793,34 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (lane == 0) TRACE(3);
                 }
 #endif
-                for (int jj = 0; jj < cnt; ++jj) {
-                    const int phys = j0 + jj < kInlineIds ? __shfl_sync(0xffffffffu, inl, jj)
-                                                          : __shfl_sync(0xffffffffu, my, jj);
-                    if (AP && it.blk0 + j0 + jj == (it.len - 1) / kTileRows)   // fused append
-                        NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
-                    const int w = (j0 + jj) % NC;
-                    int m = 0;
+                // tile j of an item goes to consumer warp j % NC; j0 is a multiple of 32, so
+                // unrolling by NC makes the warp (and its ring position) compile-time
+                for (int jj = 0; jj < cnt; jj += NC) {
 #pragma unroll
-                    for (int q = 0; q < NC; ++q)
-                        if (q == w) m = pc[q]++;
-                    if (lane == 0) {
-                        const int s = w * C::SW + m % C::SW, u = m / C::SW;
-                        if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
-                        const uint32_t bar = full0 + 8 * s;
-                        mbar_expect_tx(bar, 2 * TILE);
-                        const int row = (phys * p.num_kv_heads + it.g) * 2 * kTileRows;   // K row 0 of the tile
-                        const uint32_t dk = tiles_u + s * 2 * TILE;
-                        if (p.tma_segs == 1) {
-                            tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
-                        } else {
-                            for (int sg = 0; sg < p.tma_segs; ++sg)
-                                tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
+                    for (int w = 0; w < NC; ++w) {
+                        const int jl = jj + w;
+                        if (jl >= cnt) break;                              // warp-uniform
+                        const int phys = j0 + jl < kInlineIds ? __shfl_sync(0xffffffffu, inl, jl)
+                                                              : __shfl_sync(0xffffffffu, my, jl);
+                        if (AP && it.blk0 + j0 + jl == (it.len - 1) / kTileRows)   // fused append
+                            NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
+                        if (lane == 0) {
+                            const int s = w * C::SW + rs[w];
+                            if (ru[w] > 0) mbar_wait(empty0 + 8 * s, (ru[w] - 1) & 1);
+                            const uint32_t bar = full0 + 8 * s;
+                            mbar_expect_tx(bar, 2 * TILE);
+                            const int row = (phys * p.num_kv_heads + it.g) * 2 * kTileRows;   // K row 0 of the tile
+                            const uint32_t dk = tiles_u + s * 2 * TILE;
+                            if (p.tma_segs == 1) {
+                                tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
+                            } else {
+                                for (int sg = 0; sg < p.tma_segs; ++sg)
+                                    tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
+                            }
+                        }
+                        if (++rs[w] == C::SW) {                            // next slot of warp w's sub-ring
+                            rs[w] = 0;
+                            ++ru[w];
                         }
                     }
                 }
@@ -830,7 +839,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // ================= consumers =================
         const int wc = warp - 1;
         typename ConsumerSel<DT, G, FUSE>::T st;
-        int32_t mc = 0;                       // tiles consumed from this warp's sub-ring
+        int32_t cs = 0;                       // this warp's sub-ring position: slot, phase parity
+        uint32_t cph = 0;
         for (int k = 0;; ++k) {
             const int slot = k % IR, use = k / IR;
             mbar_wait(ifull0 + 8 * slot, use & 1);
@@ -845,9 +855,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
             __syncwarp();
             if (lane == 0) mbar_arrive(iempty0 + 8 * slot);   // item and q slot read
             for (int j = wc; j < it.nblk; j += NC) {
-                const int s = wc * C::SW + mc % C::SW, u = mc / C::SW;
-                ++mc;
-                mbar_wait(full0 + 8 * s, u & 1);
+                const int s = wc * C::SW + cs;
+                mbar_wait(full0 + 8 * s, cph);
+                if (++cs == C::SW) {                     // next slot of this warp's sub-ring
+                    cs = 0;
+                    cph ^= 1u;
+                }
 #ifdef APEX_TRACE
                 if (k == 0 && j == 0 && lane == 0 && wc == 0) TRACE(5);
 #endif
