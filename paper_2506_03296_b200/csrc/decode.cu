@@ -749,12 +749,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         // trip earlier than a load that waits for cta_begin (the list has >= grid slots)
         const WorkItem spec = p.items[blockIdx.x].it;
         const int spec_ids = lane < kInlineIds ? p.items[blockIdx.x].ids[lane] : 0;
-        // each consumer warp's sub-ring as (next slot, completed passes); incremental, so the
-        // per-tile path has no division by SW and no run-time warp index (measured: C5 +1.9%,
-        // C3 +1.2% sustained against m % SW, m / SW with the warp picked at run time)
-        int32_t rs[NC], ru[NC];
-#pragma unroll
-        for (int q = 0; q < NC; ++q) rs[q] = ru[q] = 0;
+        // lane w < NC: consumer warp w's sub-ring as (next slot, completed passes), kept
+        // incrementally -- no division by SW and no run-time warp selection on the per-tile
+        // path (measured: C5 +1.9%, C3 +1.2% sustained against m % SW, m / SW with one lane
+        // issuing for all warps; issuing from NC lanes in parallel: C2 +1.1%, others equal)
+        int32_t rs = 0, ru = 0;
+        const int hkv = p.num_kv_heads;
+        const bool one_op = p.tma_segs == 1;
         for (int k = 0;; ++k) {
             int idx;
             if (s_next < s_end) {
@@ -784,8 +785,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                 if (k == 0) TRACE(2);
             }
             const int32_t *bt = p.block_table + (size_t)it.seq * p.max_blocks_per_seq + it.blk0;
+            // lane w < NC feeds consumer warp w's sub-ring: it issues tiles j = w, w + NC, ...
+            // of the item, in order, with its own (slot, pass) counters, so the NC sub-rings
+            // are refilled in parallel and the per-tile path is one shuffle + one TMA
+            const int tl = AP ? (it.len - 1) / kTileRows - it.blk0 : -1;   // fused append: block of the new row
             for (int j0 = 0; j0 < it.nblk; j0 += 32) {
-                const int my = (j0 + lane < it.nblk && j0 + lane >= kInlineIds) ? __ldg(bt + j0 + lane) : 0;
+                const int my = j0 + lane < it.nblk ? (j0 + lane < kInlineIds ? inl : __ldg(bt + j0 + lane)) : 0;
                 const int cnt = min(32, it.nblk - j0);
 #ifdef APEX_TRACE
                 if (k == 0 && j0 == 0) {
@@ -793,34 +798,27 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
                     if (lane == 0) TRACE(3);
                 }
 #endif
-                // tile j of an item goes to consumer warp j % NC; j0 is a multiple of 32, so
-                // unrolling by NC makes the warp (and its ring position) compile-time
+                if (AP && tl >= j0 && tl < j0 + cnt)                        // warp-uniform
+                    NewRow<C::ES>::to_pool(p, it.b, it.g, __shfl_sync(0xffffffffu, my, tl - j0),
+                                           (it.len - 1) % kTileRows, lane);
                 for (int jj = 0; jj < cnt; jj += NC) {
-#pragma unroll
-                    for (int w = 0; w < NC; ++w) {
-                        const int jl = jj + w;
-                        if (jl >= cnt) break;                              // warp-uniform
-                        const int phys = j0 + jl < kInlineIds ? __shfl_sync(0xffffffffu, inl, jl)
-                                                              : __shfl_sync(0xffffffffu, my, jl);
-                        if (AP && it.blk0 + j0 + jl == (it.len - 1) / kTileRows)   // fused append
-                            NewRow<C::ES>::to_pool(p, it.b, it.g, phys, (it.len - 1) % kTileRows, lane);
-                        if (lane == 0) {
-                            const int s = w * C::SW + rs[w];
-                            if (ru[w] > 0) mbar_wait(empty0 + 8 * s, (ru[w] - 1) & 1);
-                            const uint32_t bar = full0 + 8 * s;
-                            mbar_expect_tx(bar, 2 * TILE);
-                            const int row = (phys * p.num_kv_heads + it.g) * 2 * kTileRows;   // K row 0 of the tile
-                            const uint32_t dk = tiles_u + s * 2 * TILE;
-                            if (p.tma_segs == 1) {
-                                tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
-                            } else {
-                                for (int sg = 0; sg < p.tma_segs; ++sg)
-                                    tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
-                            }
+                    const int phys = __shfl_sync(0xffffffffu, my, (jj + lane) & 31);
+                    if (lane < NC && jj + lane < cnt) {
+                        const int s = lane * C::SW + rs;
+                        if (ru > 0) mbar_wait(empty0 + 8 * s, (ru - 1) & 1);
+                        const uint32_t bar = full0 + 8 * s;
+                        mbar_expect_tx(bar, 2 * TILE);
+                        const int row = (phys * hkv + it.g) * 2 * kTileRows;   // K row 0 of the tile
+                        const uint32_t dk = tiles_u + s * 2 * TILE;
+                        if (one_op) {
+                            tma_load_3d(dk, &tmkv, bar, 0, row, 0);     // K and V of the tile, 1 op
+                        } else {
+                            for (int sg = 0; sg < p.tma_segs; ++sg)
+                                tma_load_2d(dk + sg * kSegStride, &tmkv, bar, sg * (128 / C::ES), row);
                         }
-                        if (++rs[w] == C::SW) {                            // next slot of warp w's sub-ring
-                            rs[w] = 0;
-                            ++ru[w];
+                        if (++rs == C::SW) {                            // next slot of this sub-ring
+                            rs = 0;
+                            ++ru;
                         }
                     }
                 }
