@@ -213,8 +213,8 @@ def rank_workload(w, rank, world, mode):
                     global_batch=w.batch * world, parallelism=f"req{world}" if world > 1 else "single")
     from paper_2506_03296_b200.sharding import head_range, lpt_partition
     ctx_all = w.contexts()
-    par = "single" if world == 1 else f"{mode}{world}"
-    if mode == "req" or world == 1:
+    par = "single" if world == 1 and mode != "head" else f"{mode}{world}"
+    if mode == "req" or (world == 1 and mode != "head"):
         part = lpt_partition(ctx_all, world)[rank]
         return dict(ids=np.asarray(part), ctx=ctx_all[part], hq=hq, hkv=hkv, q_off=0, kv_off=0,
                     scaling="strong", global_batch=w.batch, parallelism=par)
@@ -356,19 +356,25 @@ def run_apex(args):
     dev = torch.device("cuda", local)
     backend = args.dist_backend or ("gloo" if shared else "nccl")
     gloo = backend == "gloo"
+    w = WORKLOADS[args.config]
+    mode = resolve_mode(w, world, args.mode)
+    # --mode head at N = 1: the head-mode pipeline through a one-rank process group (the
+    # NCCL all-gather path on CUDA tensors where only one GPU is visible)
+    use_pg = world > 1 or (w.name == "c5" and mode == "head")
     if world > 1:
         if gloo:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+    elif use_pg:
+        dist.init_process_group(backend, store=dist.HashStore(), rank=0, world_size=1,
+                                **({} if gloo else {"device_id": dev}))
     coll_dev = torch.device("cpu") if gloo else dev   # where small reduction tensors live
 
     def min_over_ranks(x):
         t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return float(t.item())
-    w = WORKLOADS[args.config]
-    mode = resolve_mode(w, world, args.mode)
     wl = rank_workload(w, rank, world, mode)
     ids, ctx0 = wl["ids"], np.asarray(wl["ctx"], dtype=np.int64)
     B, hq, hkv, D, L, dt = len(ids), wl["hq"], wl["hkv"], w.head_dim, w.layers, w.dtype
@@ -580,7 +586,7 @@ def run_apex(args):
               "details": {"batch_per_gpu": B, "q_heads_per_gpu": hq, "kv_heads_per_gpu": hkv, "phys_layers": P,
                           "devices": "ranks share GPU 0 (gloo): logic check, throughput not meaningful"
                           if shared and world > 1 else f"{world} GPU(s), one rank each",
-                          "dist_backend": backend if world > 1 else None,
+                          "dist_backend": backend if use_pg else None,
                           "gather": (("fused epilogue stores + in-kernel completion flags" if fused else
                                       f"{backend} all_gather_into_tensor of head-major slices, async, overlapped "
                                       "with the next layer") if head_mode else None),
@@ -617,7 +623,7 @@ def run_apex(args):
     # ---- sampled parity + CPU oracle baseline (rank 0)
     p_last = (L - 1) % P
     ctx_now = ctx0 + (W + K - 1)                      # context of the last timed step
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not head_mode and not args.no_cpu:
         sampler = OracleSampler(w, wl, p_last, args.seed, dt, ctx_now)
         rate, t_or, o_ref, kv_tok = sampler.run(ctx_now, args.cpu_seconds)
         cores, desc = sampler.cores, sampler.describe(o_ref, ctx_now, B)
@@ -647,7 +653,7 @@ def run_apex(args):
                                   "kv_gbs": kv_tok * kv_tok_bytes / t_or / 1e9,
                                   "n_g_tokens_per_us": n_g, "n_c_tokens_per_us": n_c, "n_g_over_n_c": n_g / n_c,
                                   "cpu": _cpu_model()}
-    elif rank == 0 and world > 1 and not args.no_cpu:
+    elif rank == 0 and (world > 1 or head_mode) and not args.no_cpu:
         # sampled parity of this rank's rows (request sharding) or of the all-gathered
         # full-head output (head sharding) against the oracle over all global heads
         full_wl = dict(wl, hq=w.num_q_heads, hkv=w.num_kv_heads, q_off=0, kv_off=0)
@@ -686,7 +692,7 @@ def run_apex(args):
         if args.out:
             with open(args.out, "a") as f:
                 f.write(line + "\n")
-    if world > 1:
+    if use_pg:
         dist.barrier()
         dist.destroy_process_group()
 

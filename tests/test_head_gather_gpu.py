@@ -94,12 +94,17 @@ def _worker(rank, world, port, backend, out_dir):
     dist.destroy_process_group()
 
 
-def test_overlapped_head_gather_matches_oracle(cuda_lib, tmp_path):
+@pytest.mark.parametrize("world", [2, 1])
+def test_overlapped_head_gather_matches_oracle(cuda_lib, tmp_path, world):
+    """world 2: the sharded pipeline (NCCL with >= 2 GPUs, else gloo on one GPU);
+    world 1: the same pipeline through a one-rank NCCL group on CUDA tensors -- NCCL's
+    async all_gather_into_tensor, work.wait() and its stream ordering against the decode
+    kernels are exercised even where only one GPU is visible."""
     import torch
 
     from helpers import check_close, oracle_rows
-    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
-    mp.spawn(_worker, args=(2, _free_port(), backend, str(tmp_path)), nprocs=2, join=True)
+    backend = "nccl" if world == 1 or torch.cuda.device_count() >= 2 else "gloo"
+    mp.spawn(_worker, args=(world, _free_port(), backend, str(tmp_path)), nprocs=world, join=True)
     got = torch.load(os.path.join(str(tmp_path), "gathered.pt"))
     assert len(got) == L
     seqs = list(range(len(CTX)))
