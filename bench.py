@@ -23,7 +23,12 @@ line says so in config.devices).
 A step is one pass of the whole hot path over one batch:
 apex_kv_alloc (+1 token per request; planner + metadata upload) and, for each of
 the L logical layers, the KV append + decode attention (+ the LSE merge)
-[+ the head all-gather].  value = decode tokens/s of the whole job (one token
+[+ the head all-gather].  By default (--launch graph) the L layer-calls of a step
+are replayed from a CUDA graph captured once per step's input buffers (every
+launch parameter is step-invariant: the step's counts live in the device header
+that alloc uploads), with alloc itself eager -- the serving mode of SURVEY.md
+§8(f) f1; --launch eager issues every launch from the host.  Head sharding runs
+eager (its all-gather is issued per layer).  value = decode tokens/s of the whole job (one token
 per request per step needs all L layers) = global batch * K / max_ranks(time).
 
 Inputs are synthetic (synth/, seeded), resident in HBM before the timed region.
@@ -86,6 +91,11 @@ def parse(argv=None):
                     help="head mode: NCCL all_gather_into_tensor on head-major slices (overlapped with the next "
                          "layer), or stores into peers' symmetric memory from the decode epilogue with in-kernel "
                          "completion flags (needs >= N GPUs)")
+    ap.add_argument("--launch", choices=["graph", "eager"], default="graph",
+                    help="graph (default): each step's L per-layer calls (append + decode [+ merge]) replayed from "
+                         "a CUDA graph captured once per step's input buffers, after an eager apex_kv_alloc (host "
+                         "planner + one upload) -- the serving mode of SURVEY 8(f) f1; eager: one host call per "
+                         "launch.  Head sharding always runs eager (its gather is issued per layer)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default=None,
                     help="default nccl; gloo when the ranks share one GPU (logic check)")
     return ap.parse_args(argv)
@@ -478,7 +488,10 @@ def run_apex(args):
         epoch = [0]
     fused_append = args.append == "fused" and not head_mode   # the _ex epilogue has no append variant
     ones = [1] * B
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K * L)]
+    use_graph = args.launch == "graph" and hg is None and sg is None
+    # graph mode: the per-call events are recorded inside the captured graphs (external
+    # event-record nodes), so each decode call is still timed on the device
+    ev = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(2)] for _ in range(K * L)]
     flush, _ = l2_policy(w, wl)
     flush_buf = torch.zeros(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
@@ -490,7 +503,48 @@ def run_apex(args):
     step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     gathered = {}
 
+    graphs = {}
+
+    def layers(s, timed_idx=None):
+        qs, ks, vs = inputs[s]
+        for l in range(L):
+            p = l % P
+            if not fused_append:
+                cache.append(p, ks[p], vs[p])
+            if timed_idx is not None:
+                ev[timed_idx * L + l][0].record()
+            if fused_append:
+                cache.decode_append(p, qs[p], ks[p], vs[p], out=outs[p])
+            else:
+                cache.decode(p, qs[p], out=outs[p])
+            if timed_idx is not None:
+                ev[timed_idx * L + l][1].record()
+
+    def graph_step(s, timed_idx):
+        # every launch parameter is step-invariant (counts live in the device step header
+        # written by alloc), so a graph captured once per step's input buffers is replayed
+        # after that step's alloc; the launch count (latency vs bandwidth regime) is
+        # checked against the capture's, and a timed step whose regime changed runs eager
+        cache.alloc(seq, ones)
+        key = cache.decode_launches()
+        if (s, key) not in graphs and timed_idx is not None:
+            layers(s, timed_idx)
+            return
+        if (s, key) not in graphs:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(comp)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    layers(s)
+            comp.wait_stream(side)
+            graphs[(s, key)] = g
+        graphs[(s, key)].replay()
+
     def step(s, timed_idx=None):
+        if use_graph:
+            graph_step(s, timed_idx)
+            return
         qs, ks, vs = inputs[s]
         cache.alloc(seq, ones)
         for l in range(L):
@@ -542,6 +596,21 @@ def run_apex(args):
 
     for s in range(W):
         step(s)
+    if use_graph:
+        # capture the timed steps' graphs now (outside the timed region): their alloc
+        # is replayed by the timed step itself, so capture against the current header
+        # (the launch count is step-invariant across the run and re-checked per step)
+        key = cache.decode_launches()
+        for s2 in range(W, W + K):
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(comp)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    layers(s2, timed_idx=s2 - W)
+            comp.wait_stream(side)
+            graphs[(s2, key)] = g
+        torch.cuda.synchronize()
     n_items, n_merges = len(cache.plan()[0]), cache.plan()[1]
     decode_launches = cache.decode_launches()
     clocks = ClockSampler(local) if rank == 0 else None
@@ -590,6 +659,9 @@ def run_apex(args):
                           "gather": (("fused epilogue stores + in-kernel completion flags" if fused else
                                       f"{backend} all_gather_into_tensor of head-major slices, async, overlapped "
                                       "with the next layer") if head_mode else None),
+                          "launch": ("CUDA graph per step (the L layer-calls, captured once per step's input "
+                                     "buffers, replayed after that step's eager apex_kv_alloc; per-call events are "
+                                     "event-record nodes inside the graph)") if use_graph else "eager",
                           "work_items_per_layer": n_items, "split_merges_per_layer": n_merges,
                           "decode_launches_per_call": decode_launches,
                           "append": ("apex_decode_attention_append (latency regime: inside the decode launch; "

@@ -31,6 +31,8 @@ def main():
                             "--config", f"{c}:req:1", "--rep", rep], check=True, capture_output=True)
             shutil.copy(rep, os.path.join(prof, f"{a.tag}_{c}_decode.ncu-rep"))
     cp("bench_reference_c5.json", f"{a.tag}_c5_reference_bench.json")
+    cp("bench_c5_eager.json", f"{a.tag}_c5_eager_bench.json")
+    cp("bench_c5_head1.json", f"{a.tag}_c5_head1_nccl_bench.json")
     cp("latency_probe.jsonl", f"{a.tag}_latency_probe_final.jsonl")
     cp("gpus2_head.json", f"{a.tag}_gpus2_head_same_gpu.json")
     cp("gpus2_req.json", f"{a.tag}_gpus2_req_same_gpu.json")

@@ -12,6 +12,8 @@ timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "py
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err; echo "bench c5 rc=$?"
 timeout 600 python bench.py --impl reference > $O/bench_reference_c5.json 2> $O/bench_reference_c5.err; echo "ref rc=$?"
+timeout 900 python bench.py --launch eager --no-cpu > $O/bench_c5_eager.json 2> $O/bench_c5_eager.err; echo "bench c5 eager rc=$?"
+timeout 900 python bench.py --mode head --no-cpu > $O/bench_c5_head1.json 2> $O/bench_c5_head1.err; echo "bench c5 head1 rc=$?"
 for c in c3 c1 c2 c4; do
   timeout 600 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench $c rc=$?"
 done
