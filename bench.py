@@ -418,7 +418,7 @@ def run_apex(args):
                          max_new_tokens=max(chunk_rows, B) + int(ctx0.max()), dtype=dt, device=dev)
     if args.sched is not None:
         cache.set_sched(args.sched)
-    seq = list(range(B))                              # handle-local sequence ids = batch rows
+    seq = np.arange(B, dtype=np.int32)                # handle-local sequence ids = batch rows
     gid = torch.as_tensor(ids.astype(np.int32), device=dev)
 
     # ---- prefill positions 0..ctx-2 through the C ABI (alloc + append), chunked by rows
@@ -487,7 +487,7 @@ def run_apex(args):
         sig_status = torch.zeros(1, dtype=torch.int32, device=dev)
         epoch = [0]
     fused_append = args.append == "fused" and not head_mode   # the _ex epilogue has no append variant
-    ones = [1] * B
+    ones = np.ones(B, dtype=np.int32)
     use_graph = args.launch == "graph" and hg is None and sg is None
     # graph mode: the per-call events are recorded inside the captured graphs (external
     # event-record nodes), so each decode call is still timed on the device
@@ -805,7 +805,7 @@ def run_e2e(args, cache, inputs, seq, B, hq, hkv, D, L, P, tdt, dev, hg, fused_a
         e.record(comp)
 
     def e2e_step():
-        cache.alloc(seq, [1] * B)
+        cache.alloc(seq, np.ones(B, dtype=np.int32))
         for l in range(L):
             p, j = l % P, l % NB
             with torch.cuda.stream(h2d_s):

@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", src, "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *ARCH, *HOST_FLAGS, "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *HOST_FLAGS, *["-D" + d for d in defines], "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

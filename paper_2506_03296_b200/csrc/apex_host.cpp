@@ -22,6 +22,10 @@
 
 #include "apex_internal.h"
 
+#ifndef APEX_UPLOAD_KERNEL
+#define APEX_UPLOAD_KERNEL 1   // 0: cudaMemcpyAsync of the step metadata + the delta kernel
+#endif
+
 using apex::MergeItem;
 using apex::WorkItem;
 
@@ -239,9 +243,25 @@ struct apex_kv {
 
     // pinned staging ring for the per-step upload
     uint8_t *staging[2] = {nullptr, nullptr};
+    uint8_t *staging_dev[2] = {nullptr, nullptr};   // device view of the mapped staging buffers
     cudaEvent_t staged[2] = {nullptr, nullptr};
     bool staged_pending[2] = {false, false};
     int ring = 0;
+
+    // per-step scratch, reused across calls so a step allocates nothing once warm
+    // (large std::vectors freed and re-grown every step went back to mmap and page
+    // faults: ~2 ms of host time per C5 alloc).  Never observable state: the
+    // all-or-nothing contract concerns the fields above.
+    struct Scratch {
+        std::vector<int32_t> seen, lens, seq_of_row, nblks, pc, cnt, slots, popped;
+        std::vector<int2> bt_delta, len_delta;
+        std::vector<WorkItem> dyn, items, plan_items;   // queue, sort scratch, spare plan storage
+        std::vector<MergeItem> merges;                   // spare plan storage
+        std::vector<int32_t> cta_begin;                  // spare plan storage
+        std::vector<Seq> before;
+        int32_t stamp = 0;
+    };
+    mutable Scratch sc;
 
     std::vector<apex::TmaMap> tmaps;
     int tma_segs = 1;   // 1: 3-D map (one op per tile); else ops per tile with the 2-D map
@@ -282,7 +302,9 @@ apex_status apex_kv_create(const apex_kv_desc *desc, apex_kv **out) {
         kv->kv_pools.assign(desc->kv_pool, desc->kv_pool + desc->num_layers);
         kv->d.kv_pool = kv->kv_pools.data();
         for (int i = 0; i < 2; ++i) {
-            cudaError_t e = cudaHostAlloc((void **)&kv->staging[i], kv->ws.upload_cap, cudaHostAllocDefault);
+            // mapped: the upload kernel reads the step metadata straight from it (zero-copy)
+            cudaError_t e = cudaHostAlloc((void **)&kv->staging[i], kv->ws.upload_cap, cudaHostAllocMapped);
+            if (e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&kv->staging_dev[i], kv->staging[i], 0);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->staged[i], cudaEventDisableTiming);
             if (e != cudaSuccess) {
                 apex_kv_destroy(kv);
@@ -517,7 +539,8 @@ static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_
     const int64_t P = std::max<int64_t>(1, kv->grid_override > 0
                                                ? kv->grid_override
                                                : apex::decode_grid_ctas(kv->d.dtype, kv->group, kv->sm_count));
-    std::vector<int32_t> nblks(B);
+    std::vector<int32_t> &nblks = kv->sc.nblks;
+    nblks.resize(B);
     int64_t T = 0;
 
     for (int32_t b = 0; b < B; ++b) {
@@ -538,20 +561,34 @@ static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_
         // t_tile ~ 0.34 us (8 KiB at a CTA's share of HBM), t_item ~ 3 us (per-item
         // cost incl. the split's merge share; fitted on batch 128 x 512: whole pairs
         // 63.5 us vs halves 70.7 us), in units of 0.01 us.
-        int32_t maxn = 1;
-        for (int32_t b = 0; b < B; ++b) maxn = std::max(maxn, nblks[b]);
+        // the model depends on the lengths only through their distinct values (counted),
+        // and many candidates coincide: evaluate each distinct candidate once over the
+        // distinct lengths (host time of a uniform batch-256 plan: ~150 -> ~10 us)
+        std::vector<int32_t> &uv = kv->sc.cnt;                 // sorted lengths -> (value, count) pairs
+        uv.assign(nblks.begin(), nblks.end());
+        std::sort(uv.begin(), uv.end());
+        std::vector<std::pair<int32_t, int64_t>> hist;
+        for (size_t i = 0; i < uv.size();) {
+            size_t j = i;
+            while (j < uv.size() && uv[j] == uv[i]) ++j;
+            hist.push_back({uv[i], (int64_t)(j - i)});
+            i = j;
+        }
+        const int32_t maxn = std::max<int32_t>(1, hist.back().first);
         auto cost = [&](int64_t c) {
             int64_t n = 0, big = 0;
-            for (int32_t b = 0; b < B; ++b) {
-                const int64_t k = cdiv(nblks[b], c);
-                n += k * Hkv;
-                big = std::max(big, cdiv(nblks[b], k));
+            for (const auto &h : hist) {
+                const int64_t k = cdiv(h.first, c);
+                n += k * Hkv * h.second;
+                big = std::max(big, cdiv(h.first, k));
             }
             return cdiv(n, P) * (big * 34 + 300);
         };
         std::vector<int64_t> cand;
         for (int64_t k = 1; k <= 64; ++k) cand.push_back(cdiv(maxn, k));
         for (int64_t r = 1; r <= 16; ++r) cand.push_back(std::max<int64_t>(1, cdiv(T, P * r)));
+        std::sort(cand.begin(), cand.end(), std::greater<int64_t>());   // larger chunk first: ties keep it
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
         int64_t best = -1;
         chunk = maxn;
         for (int64_t c : cand) {
@@ -567,63 +604,89 @@ static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_
     } else {
         chunk = std::max<int64_t>(16, cdiv(T, 16 * P));   // >= 16 tiles: per-item costs stay small
     }
-    // pieces of every (row, kv head) pair, in pair order
-    std::vector<std::vector<Piece>> pair_pieces;
+    // pieces of every (row, kv head) pair, in pair order -> work items (+ merges of split pairs)
+    std::vector<std::vector<WorkItem>> st_items(streamk ? P : 0);
+    std::vector<WorkItem> &dyn = kv->sc.dyn;
+    std::vector<MergeItem> &merges = out.merges;
+    dyn.clear();
+    merges.clear();
+    int32_t parts = 0;
+    size_t n_items = 0;
+    auto emit = [&](int32_t b, int32_t g, const Piece *pp, size_t np) {
+        const bool split = np > 1;
+        const int32_t mg = split ? (int32_t)merges.size() : -1;
+        if (split) merges.push_back({b, g, parts, (int32_t)np});
+        for (size_t i = 0; i < np; ++i) {
+            const WorkItem w{b, g, pp[i].blk0, pp[i].nblk, split ? parts + (int32_t)i : -1, seq_of_row[b], lens[b],
+                             mg};
+            (pp[i].cta >= 0 ? st_items[pp[i].cta] : dyn).push_back(w);
+        }
+        if (split) parts += (int32_t)np;
+        n_items += np;
+    };
     if (streamk) {
+        std::vector<std::vector<Piece>> pair_pieces;
         plan_streamk(nblks, Hkv, P, T, kv->dyn_permille, pair_pieces);
+        for (int32_t b = 0; b < B; ++b)
+            for (int32_t g = 0; g < Hkv; ++g) {
+                const auto &pp = pair_pieces[(size_t)b * Hkv + g];
+                emit(b, g, pp.data(), pp.size());
+            }
     } else {
-        pair_pieces.assign((size_t)B * Hkv, {});
-        std::vector<int32_t> pc;
+        std::vector<int32_t> &pc = kv->sc.pc;
+        std::vector<Piece> pcs;
         // guided (apex_kv_set_sched(-2)): the pairs holding the last fractions of the
         // tiles (flattened order) are cut into halved, quartered, ... chunks, so the
         // queue (longest first) ends with small items and the CTAs finish together
         const bool guided = !latency && kv->forced_chunk_blocks == 0 && kv->dyn_permille == -2;
         if (guided) chunk = std::max<int64_t>(16, cdiv(T, (int64_t)kv->guided[0] * P));
-        int64_t pos = 0;
+        int64_t pos = 0, last_c = -1;
+        int32_t last_n = -1;
         for (int32_t b = 0; b < B; ++b) {
             for (int32_t g = 0; g < Hkv; ++g) {
                 if (g == 0 || guided) {
                     int64_t c = chunk;
                     for (int k = 1; guided && k < 4; ++k)
                         if (pos * 1000 >= (int64_t)kv->guided[k] * T) c = std::max<int64_t>(8, chunk >> k);
-                    pieces_of(nblks[b], c, pc);
+                    if (c != last_c || nblks[b] != last_n) {   // pieces depend on (length, chunk) only
+                        pieces_of(nblks[b], c, pc);
+                        pcs.clear();
+                        int32_t blk = 0;
+                        for (int32_t n : pc) {
+                            pcs.push_back({-1, blk, n});
+                            blk += n;
+                        }
+                        last_c = c;
+                        last_n = nblks[b];
+                    }
                 }
                 pos += nblks[b];
-                int32_t blk = 0;
-                for (int32_t n : pc) {
-                    pair_pieces[(size_t)b * Hkv + g].push_back({-1, blk, n});
-                    blk += n;
-                }
+                emit(b, g, pcs.data(), pcs.size());
             }
+            if ((int64_t)n_items > kv->ws.max_items) break;   // reported below; stop growing
         }
     }
-    std::vector<std::vector<WorkItem>> st_items(streamk ? P : 0);
-    std::vector<WorkItem> dyn;
-    std::vector<MergeItem> merges;
-    int32_t parts = 0;
-    size_t n_items = 0;
-    for (int32_t b = 0; b < B; ++b)
-        for (int32_t g = 0; g < Hkv; ++g) {
-            const auto &pp = pair_pieces[(size_t)b * Hkv + g];
-            const bool split = pp.size() > 1;
-            const int32_t mg = split ? (int32_t)merges.size() : -1;
-            if (split) merges.push_back({b, g, parts, (int32_t)pp.size()});
-            for (size_t i = 0; i < pp.size(); ++i) {
-                const WorkItem w{b, g, pp[i].blk0, pp[i].nblk, split ? parts + (int32_t)i : -1, seq_of_row[b],
-                                 lens[b], mg};
-                (pp[i].cta >= 0 ? st_items[pp[i].cta] : dyn).push_back(w);
-            }
-            if (split) parts += (int32_t)pp.size();
-            n_items += pp.size();
-        }
     if ((int64_t)n_items > kv->ws.max_items)
-        return fail(APEX_EINVAL, "split chunk of %lld tokens yields %zu work items > workspace capacity %d",
-                    (long long)chunk * kv->d.block_size, n_items, kv->ws.max_items);
-    std::stable_sort(dyn.begin(), dyn.end(), [](const WorkItem &a, const WorkItem &b) { return a.nblk > b.nblk; });
+        return fail(APEX_EINVAL, "split chunk of %lld tokens yields %s%zu work items > workspace capacity %d",
+                    (long long)chunk * kv->d.block_size, streamk ? "" : "at least ", n_items, kv->ws.max_items);
     std::vector<WorkItem> &items = out.items;
     items.clear();
     items.reserve(n_items);
     out.cta_begin.assign((size_t)P + 1, 0);
+    // the dynamic queue longest-first: a stable counting sort on nblk (descending),
+    // identical to std::stable_sort with a.nblk > b.nblk, O(items + max nblk)
+    std::vector<WorkItem> &sorted = kv->sc.items;
+    {
+        int32_t mx = 0;
+        for (const WorkItem &w : dyn) mx = std::max(mx, w.nblk);
+        std::vector<int32_t> &cnt = kv->sc.cnt;
+        cnt.assign((size_t)mx + 2, 0);
+        for (const WorkItem &w : dyn) ++cnt[(size_t)(mx - w.nblk) + 1];
+        for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+        sorted.resize(dyn.size());
+        for (const WorkItem &w : dyn) sorted[(size_t)cnt[(size_t)(mx - w.nblk)]++] = w;
+        dyn.swap(sorted);
+    }
     if (streamk) {
         for (int64_t c = 0; c < P; ++c) {
             out.cta_begin[c] = (int32_t)items.size();
@@ -646,16 +709,22 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     if (!seq_ids || !n_new || n < 1 || n > kv->d.max_batch)
         return fail(APEX_EINVAL, "batch of %d sequences not in [1, max_batch=%d]", n, kv->d.max_batch);
     const int32_t bs = kv->d.block_size;
+    auto &sc = kv->sc;
     // ---- 1. validate, plan and size the upload on the would-be lengths, before touching
     // any state: every failure below leaves the handle exactly as it was (all-or-nothing)
-    std::vector<char> seen(kv->d.max_seqs, 0);
-    std::vector<int32_t> lens(n);
+    if (sc.seen.size() != (size_t)kv->d.max_seqs || sc.stamp == INT32_MAX) {
+        sc.seen.assign(kv->d.max_seqs, 0);
+        sc.stamp = 0;
+    }
+    const int32_t stamp = ++sc.stamp;                 // "seen in this call" = seen[s] == stamp
+    std::vector<int32_t> &lens = sc.lens;
+    lens.resize(n);
     int64_t need = 0, rows = 0;
     for (int32_t i = 0; i < n; ++i) {
         const int32_t s = seq_ids[i], k = n_new[i];
         if (s < 0 || s >= kv->d.max_seqs) return fail(APEX_EINVAL, "seq id %d out of range", s);
-        if (seen[s]) return fail(APEX_EINVAL, "seq id %d repeated in one alloc", s);
-        seen[s] = 1;
+        if (sc.seen[s] == stamp) return fail(APEX_EINVAL, "seq id %d repeated in one alloc", s);
+        sc.seen[s] = stamp;
         if (k < 0) return fail(APEX_EINVAL, "n_new[%d] = %d < 0", i, k);
         const int64_t L = kv->seqs[s].live ? kv->seqs[s].len : 0;
         if (L + k < 1) return fail(APEX_EINVAL, "seq %d would have an empty context (reading c4)", s);
@@ -669,8 +738,23 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         return fail(APEX_EINVAL, "%lld new tokens > max_new_tokens %d", (long long)rows, kv->d.max_new_tokens);
     if (need > (int64_t)kv->free_stack.size())
         return fail(APEX_ENOBLOCKS, "need %lld blocks, %zu free", (long long)need, kv->free_stack.size());
-    std::vector<int32_t> seq_of_row(seq_ids, seq_ids + n);
+    std::vector<int32_t> &seq_of_row = sc.seq_of_row;
+    seq_of_row.assign(seq_ids, seq_ids + n);
+    // the plan is built in spare storage kept by the handle; whatever the exit path, the
+    // storage that is not committed goes back to the spares (no per-step allocations)
     Plan plan;
+    plan.items.swap(sc.plan_items);
+    plan.merges.swap(sc.merges);
+    plan.cta_begin.swap(sc.cta_begin);
+    struct Spares {
+        apex_kv::Scratch &sc;
+        Plan &p;
+        ~Spares() {
+            sc.plan_items.swap(p.items);
+            sc.merges.swap(p.merges);
+            sc.cta_begin.swap(p.cta_begin);
+        }
+    } spares{sc, plan};
     apex_status st = plan_step(kv, seq_of_row, lens, plan);
     if (st != APEX_OK) return st;
     // packed upload: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
@@ -693,11 +777,16 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     }
 
     // ---- 2. commit: pop blocks, compute slots and deltas (cannot fail)
-    std::vector<int32_t> slots;
+    std::vector<int32_t> &slots = sc.slots;
+    slots.clear();
     slots.reserve(rows);
-    std::vector<int2> bt_delta, len_delta;
-    std::vector<int32_t> popped;                       // pop order (for the CUDA-failure rollback)
-    std::vector<apex_kv::Seq> before(n);               // (live, len) of each seq before the call
+    std::vector<int2> &bt_delta = sc.bt_delta, &len_delta = sc.len_delta;
+    bt_delta.clear();
+    len_delta.clear();
+    std::vector<int32_t> &popped = sc.popped;          // pop order (for the CUDA-failure rollback)
+    popped.clear();
+    std::vector<apex_kv::Seq> &before = sc.before;     // (live, len) of each seq before the call
+    if (before.size() < (size_t)n) before.resize(n);
     for (int32_t i = 0; i < n; ++i) {
         auto &sq = kv->seqs[seq_ids[i]];
         before[i].live = sq.live;
@@ -756,6 +845,17 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         std::memcpy(host + o_len, len_delta.data(), sizeof(int2) * len_delta.size());
         uint8_t *dev = (uint8_t *)kv->d.workspace + kv->ws.upload;
         cudaStream_t s = (cudaStream_t)stream;
+#if APEX_UPLOAD_KERNEL
+        // ONE launch: copy the metadata from the mapped staging buffer into the device
+        // upload region and apply the table / length deltas from the same host copy
+        // (an H2D copy + the delta kernel cost two serialised operations per step)
+        const uint8_t *hdev = kv->staging_dev[r];
+        cudaError_t e = apex::launch_upload(hdev, dev, up_end, (const int2 *)(hdev + o_bt), (int)bt_delta.size(),
+                                            (const int2 *)(hdev + o_len), (int)len_delta.size(), kv->d.block_table,
+                                            kv->d.seq_lens, kv->sm_count, s);
+        if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
+        if (e == cudaSuccess) kv->staged_pending[r] = true;
+#else
         cudaError_t e = cudaMemcpyAsync(dev, host, up_end, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaEventRecord(kv->staged[r], s);
         if (e == cudaSuccess) {
@@ -764,6 +864,7 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
                                           (const int2 *)(dev + o_len), (int)len_delta.size(), kv->d.block_table,
                                           kv->d.seq_lens, s);
         }
+#endif
         if (e != cudaSuccess) {
             rollback();
             // the device header may already hold the withdrawn step: append/decode are

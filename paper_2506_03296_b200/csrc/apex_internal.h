@@ -110,6 +110,9 @@ struct TmaMap {
 apex_status set_error(apex_status st, const char *fmt, ...);
 
 // launchers: return cudaSuccess or the launch error
+cudaError_t launch_upload(const void *host_src, void *dev_dst, size_t bytes, const int2 *bt_delta, int n_bt,
+                          const int2 *len_delta, int n_len, int32_t *block_table, int32_t *seq_lens, int sm_count,
+                          cudaStream_t s);
 cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
                                 int32_t *block_table, int32_t *seq_lens, cudaStream_t s);
 cudaError_t launch_append(apex_dtype dt, const void *k_new, const void *v_new, void *kv_pool,

@@ -48,7 +48,38 @@ __global__ void apex_apply_deltas_kernel(const int2 *__restrict__ bt_delta, int 
     }
 }
 
+// One launch instead of an H2D copy + the delta kernel: the step metadata is read
+// straight from the mapped pinned staging buffer (zero-copy over PCIe) into the device
+// upload region, and the table / length deltas are applied from the same host copy.
+__global__ void apex_upload_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int n16,
+                                   const int2 *__restrict__ bt_delta, int n_bt, const int2 *__restrict__ len_delta,
+                                   int n_len, int32_t *__restrict__ block_table, int32_t *__restrict__ seq_lens) {
+    const int nth = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16 + n_bt + n_len; i += nth) {
+        if (i < n16) {
+            dst[i] = src[i];
+        } else if (i < n16 + n_bt) {
+            const int2 d = bt_delta[i - n16];
+            block_table[d.x] = d.y;
+        } else {
+            const int2 d = len_delta[i - n16 - n_bt];
+            seq_lens[d.x] = d.y;
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_upload(const void *host_src, void *dev_dst, size_t bytes, const int2 *bt_delta, int n_bt,
+                          const int2 *len_delta, int n_len, int32_t *block_table, int32_t *seq_lens, int sm_count,
+                          cudaStream_t s) {
+    const int n16 = (int)(bytes / 16);
+    const int n = n16 + n_bt + n_len;
+    const int blocks = (n + 255) / 256 < 2 * sm_count ? (n + 255) / 256 : 2 * sm_count;
+    apex_upload_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint4 *>(host_src), static_cast<uint4 *>(dev_dst), n16,
+                                               bt_delta, n_bt, len_delta, n_len, block_table, seq_lens);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_apply_deltas(const int2 *bt_delta, int n_bt, const int2 *len_delta, int n_len,
                                 int32_t *block_table, int32_t *seq_lens, cudaStream_t s) {
@@ -77,6 +108,7 @@ cudaError_t append_prepare() {
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, apex_append_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, apex_apply_deltas_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, apex_upload_kernel);
     return e;
 }
 

@@ -11,6 +11,8 @@ import contextlib
 import ctypes
 import math
 
+import numpy as np
+
 from . import apex as A
 
 _TORCH_DT = {"f32": "float32", "f16": "float16", "bf16": "bfloat16"}
@@ -94,8 +96,8 @@ class PagedKVCache:
     def alloc(self, seq_ids, n_new):
         with self._on_device():
             A.apex_kv_alloc(self.handle, seq_ids, n_new, self._stream())
-        self.batch_seq_ids = [int(s) for s in seq_ids]
-        self.n_rows = int(sum(int(x) for x in n_new))
+        self.batch_seq_ids = np.asarray(seq_ids, dtype=np.int64).tolist()
+        self.n_rows = int(np.asarray(n_new, dtype=np.int64).sum())
 
     def release(self, seq_id: int):
         A.apex_kv_release(self.handle, seq_id)

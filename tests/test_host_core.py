@@ -175,7 +175,42 @@ def _check_plan(c, lens, hkv, bs=16):
     assert cb[0] == 0 and all(cb[i] <= cb[i + 1] for i in range(len(cb) - 1)) and cb[-1] <= len(items)
     dyn = items[cb[-1]:]
     assert all(dyn[i][3] >= dyn[i + 1][3] for i in range(len(dyn) - 1))
+    # stable: equal-length queue items keep their (row, kv head, block) emission order
+    assert all(dyn[i][:3] < dyn[i + 1][:3] for i in range(len(dyn) - 1) if dyn[i][3] == dyn[i + 1][3])
     return items, n_merges
+
+
+def test_plan_is_a_function_of_the_lengths_across_steps():
+    """The planner reuses scratch storage across apex_kv_alloc calls; a long-lived
+    handle whose batches grow, shrink and change regime must produce, every step,
+    exactly the plan a fresh handle makes for the same lengths."""
+    rnd = random.Random(5)
+    kw = dict(num_q_heads=32, num_kv_heads=8, num_blocks=1 << 15, max_blocks_per_seq=1024, max_seqs=300,
+              max_batch=300, dtype="bf16", max_new_tokens=1 << 20)
+    live = host_cache(**kw)
+    lens = {}
+    for step in range(25):
+        B = rnd.choice([1, 3, 40, 257, 300])
+        seqs = sorted(rnd.sample(range(300), B))
+        new = [rnd.randint(1, 3000) if s not in lens else rnd.choice([1, 1, 16]) for s in seqs]
+        if sum(-(-(lens.get(s, 0) + n) // 16) - -(-lens.get(s, 0) // 16) for s, n in zip(seqs, new)) > \
+                live.num_free_blocks():
+            for s in list(lens):
+                live.release(s)
+            lens.clear()
+            new = [rnd.randint(1, 3000) for _ in seqs]
+        live.alloc(seqs, new)
+        for s, n in zip(seqs, new):
+            lens[s] = lens.get(s, 0) + n
+        fresh = host_cache(**kw)
+        fresh.alloc(list(range(B)), [lens[s] for s in seqs])
+        got, want = live.plan(), fresh.plan()
+        # identical up to the sequence ids (the fresh handle numbers the rows 0..B-1)
+        assert got[1] == want[1] and len(got[0]) == len(want[0])
+        for a, b in zip(got[0], want[0]):
+            assert a[:5] == b[:5] and a[5] == seqs[b[5]]
+        assert live.plan_ranges() == fresh.plan_ranges()
+        fresh.close()
 
 
 def test_planner_coverage_random():
