@@ -80,6 +80,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=30.0,
+                    help="--impl reference: oracle seconds for the whole run (bounded sample per step)")
     ap.add_argument("--out", default="")
     ap.add_argument("--append", choices=["fused", "separate"], default="fused",
                     help="fused: apex_decode_attention_append (append inside the decode launch in the latency "
@@ -322,7 +324,7 @@ def run_reference(args):
     ctx = np.asarray(wl["ctx"], dtype=np.int64)
     S = args.warmup + args.steps
     sampler = OracleSampler(w, wl, 0, args.seed, w.dtype, ctx + S)
-    per_step = max(0.5, 30.0 / max(S, 1))           # bounded: ~30 s of oracle time for the whole run
+    per_step = max(0.1, args.ref_seconds / max(S, 1))   # bounded: ~30 s of oracle time for the whole run
     rates, step_s_list, desc, t_total = [], [], "", 0.0
     for s in range(S):
         ctx_s = ctx + s
@@ -345,7 +347,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"per step: {desc}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit_line(json.dumps(line))
 
 
 # ------------------------------------------------------------------ apex arm
@@ -760,7 +762,7 @@ def run_apex(args):
         hg.close()
     if rank == 0:
         line = json.dumps(result)
-        print(line, flush=True)
+        emit_line(line)
         if args.out:
             with open(args.out, "a") as f:
                 f.write(line + "\n")
@@ -945,10 +947,27 @@ def self_launch(args):
     return subprocess.call(cmd, env=env)
 
 
+_JSON_OUT = None
+
+
+def emit_line(line: str):
+    """The one JSON line, to the real stdout (see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(line + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args))
+    # stdout carries only the JSON line: libraries write to fd 1 directly (NCCL prints its
+    # version banner there when its communicator comes up), so fd 1 is pointed at stderr
+    # for the run and the line goes to a saved copy of the original stdout
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
     else:

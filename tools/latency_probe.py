@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--sched", type=int, default=None, help="apex_kv_set_sched value")
     ap.add_argument("--lat-tiles", type=int, default=512, help="apex_kv_set_planner latency_tiles_per_cta")
     ap.add_argument("--graph", action="store_true", help="time a CUDA-graph replay of the call")
+    ap.add_argument("--split", type=int, default=0, help="apex_kv_set_split chunk in tokens (0: planner)")
     ap.add_argument("--flush", choices=["read", "write"], default="read",
                     help="L2 flush before each call: read a 512 MiB buffer (L2 left clean) or write it (L2 left "
                          "full of dirty lines whose write-back competes with the decode's reads)")
@@ -48,6 +49,8 @@ def main():
         cache.set_planner(a.lat_tiles)
         if a.sched is not None:
             cache.set_sched(a.sched)
+        if a.split:
+            cache.set_split(a.split)
         cache.alloc(seqs, [1] * batch)
         k = gen_dev(cache, 1, 0, seqs, [ctx] * batch, hkv)
         cache.append(0, k, k)
@@ -82,7 +85,7 @@ def main():
         print(json.dumps({"dtype": dtype, "hq": hq, "hkv": hkv, "batch": batch, "ctx": ctx + 1, "us": round(us, 2),
                           "us_min": round(min(times), 2), "items": len(cache.plan()[0]),
                           "launches": cache.decode_launches(), "gbs": round(kv / us / 1e3, 1),
-                          "sched": a.sched, "lat_tiles": a.lat_tiles, "graph": a.graph,
+                          "sched": a.sched, "lat_tiles": a.lat_tiles, "split": a.split, "graph": a.graph,
                           "flush": a.flush}), flush=True)
         cache.close()
         del cache
