@@ -233,12 +233,12 @@ apex_status apex_kv_set_grid(apex_kv *kv, int32_t ctas);
    Default: the automatic choice documented in DESIGN.md.  APEX_EINVAL outside
    [-2, 1000]. */
 apex_status apex_kv_set_sched(apex_kv *kv, int32_t dyn_permille);
-/* Planner constants (tuning; defaults 512, 8, 900, 950, 980), used by the NEXT
+/* Planner constants (tuning; defaults 512, 4, 900, 950, 980), used by the NEXT
    apex_kv_alloc: the latency regime (fused in-kernel merge, one launch) applies
    while total tiles T <= latency_tiles_per_cta * grid (0 disables it); the guided
-   bandwidth split cuts items of ceil(T / (guided_div * grid)) blocks, halved /
-   quartered / eighthed for the pairs holding the last (1000 - pm1), (1000 - pm2),
-   (1000 - pm3) permille of the tiles.  APEX_EINVAL (nothing changed) unless
+   bandwidth split cuts items of ceil(T / (guided_div * grid)) blocks, and, for the
+   pairs holding the last (1000 - pm1), (1000 - pm2), (1000 - pm3) permille of the
+   tiles, items of 1/2, 1/4, 1/8 of ceil(T / (max(guided_div, 8) * grid)) blocks.  APEX_EINVAL (nothing changed) unless
    0 <= latency_tiles_per_cta <= 2^20, 1 <= guided_div <= 64 and
    0 <= pm1 <= pm2 <= pm3 <= 1000. */
 apex_status apex_kv_set_planner(apex_kv *kv, int32_t latency_tiles_per_cta, int32_t guided_div, int32_t guided_pm1,

@@ -221,7 +221,10 @@ struct apex_kv {
     int32_t grid_override = 0;
     int32_t dyn_permille = kDefaultDynPermille;   // apex_kv_set_sched
     int64_t latency_tiles_per_cta = 512;          // latency regime while T <= this * P
-    int32_t guided[4] = {8, 900, 950, 980};       // guided: T/(g0 P) chunk, halved from permille g1, g2, g3
+    // guided: T/(g0 P) bulk chunk; from permille g1, g2, g3 the halves, quarters, eighths of
+    // T/(max(g0, 8) P).  g0 = 4 (was 8, same tail): C2 -0.95%, C3 -0.9%, C4/C5 +-0.05% per
+    // call, same box (profiles/r02_guided_div/)
+    int32_t guided[4] = {4, 900, 950, 980};
     int32_t plan_grid = 0;                        // CTAs the last plan was made for (= launch grid)
     std::vector<int32_t> cta_begin;               // [plan_grid + 1]
 
@@ -639,7 +642,14 @@ static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_
         // tiles (flattened order) are cut into halved, quartered, ... chunks, so the
         // queue (longest first) ends with small items and the CTAs finish together
         const bool guided = !latency && kv->forced_chunk_blocks == 0 && kv->dyn_permille == -2;
-        if (guided) chunk = std::max<int64_t>(16, cdiv(T, (int64_t)kv->guided[0] * P));
+        // bulk pieces of T/(g0 P) tiles; the tail pieces halve from T/(max(g0, 8) P), so a
+        // small g0 keeps the bulk pairs whole (fewer items and split pairs) while the end of
+        // the queue stays as fine as with g0 = 8 (identical plans for g0 >= 8)
+        int64_t tail_base = chunk;
+        if (guided) {
+            chunk = std::max<int64_t>(16, cdiv(T, (int64_t)kv->guided[0] * P));
+            tail_base = std::max<int64_t>(16, cdiv(T, (int64_t)std::max<int32_t>(kv->guided[0], 8) * P));
+        }
         int64_t pos = 0, last_c = -1;
         int32_t last_n = -1;
         for (int32_t b = 0; b < B; ++b) {
@@ -647,7 +657,7 @@ static apex_status plan_step(const apex_kv *kv, const std::vector<int32_t> &seq_
                 if (g == 0 || guided) {
                     int64_t c = chunk;
                     for (int k = 1; guided && k < 4; ++k)
-                        if (pos * 1000 >= (int64_t)kv->guided[k] * T) c = std::max<int64_t>(8, chunk >> k);
+                        if (pos * 1000 >= (int64_t)kv->guided[k] * T) c = std::max<int64_t>(8, tail_base >> k);
                     if (c != last_c || nblks[b] != last_n) {   // pieces depend on (length, chunk) only
                         pieces_of(nblks[b], c, pc);
                         pcs.clear();

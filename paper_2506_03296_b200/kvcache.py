@@ -207,7 +207,7 @@ class PagedKVCache:
         that permille of the tiles left to the dynamic queue (bandwidth regime)."""
         A.apex_kv_set_sched(self.handle, dyn_permille)
 
-    def set_planner(self, latency_tiles_per_cta: int = 512, guided_div: int = 8, guided_pm=(900, 950, 980)):
+    def set_planner(self, latency_tiles_per_cta: int = 512, guided_div: int = 4, guided_pm=(900, 950, 980)):
         """Planner constants (tuning aid; include/apex.h apex_kv_set_planner)."""
         A.apex_kv_set_planner(self.handle, latency_tiles_per_cta, guided_div, *guided_pm)
 

@@ -340,7 +340,7 @@ def test_planner_choice_at_config_scale():
     c5.alloc(list(range(1024)), [1] * 1024)
     dt = time.perf_counter() - t0
     items, nm = c5.plan()
-    # guided (default): chunk T/(8P) = 3547 blocks > 1025, so the first 90% of the pairs
+    # guided (default): chunk T/(4P) = 7094 blocks > 1025, so the first 90% of the pairs
     # (flattened order) stay whole; only the last 5% / 2% are cut (in 2 / 3 pieces)
     whole = {(it[0], it[1]) for it in items if it[4] < 0}
     assert len(whole) == 8192 - nm and nm <= 0.1 * 8192 and nm > 0
@@ -356,11 +356,17 @@ def test_planner_choice_at_config_scale():
     c3.set_grid(296)
     c3.alloc(list(range(128)), [8192] * 128)
     items, nm = _check_plan(c3, [8192] * 128, 8)
-    # guided: chunk ceil(T/8P) = 222 blocks -> 3 pieces of 171; the last 10 / 5 / 2% of the
-    # pairs use chunks 111 / 55 / 27 -> 5 / 10 / 19 pieces, run last (longest first)
+    # guided: bulk chunk ceil(T/4P) = 443 blocks -> 2 pieces of 256; the last 10 / 5 / 2% of
+    # the pairs use chunks 111 / 55 / 27 (halves of ceil(T/8P) = 222) -> 5 / 10 / 19 pieces,
+    # run last (longest first)
     sizes = sorted({it[3] for it in items})
-    assert nm == 1024 and max(sizes) == 171 and min(sizes) <= 27
-    assert items[0][3] == 171 and items[-1][3] == min(sizes)
+    assert nm == 1024 and max(sizes) == 256 and min(sizes) <= 27
+    assert items[0][3] == 256 and items[-1][3] == min(sizes)
+    c3.set_planner(512, 8, (900, 950, 980))          # g0 = 8 (the round-1 default): 3 pieces of 171
+    c3.alloc(list(range(128)), [0] * 128)
+    items, nm = c3.plan()
+    assert nm == 1024 and max(it[3] for it in items) == 171
+    c3.set_planner()
     c3.set_sched(-1)
     c3.alloc(list(range(128)), [1] * 128)
     items, nm = _check_plan(c3, [8193] * 128, 8)
