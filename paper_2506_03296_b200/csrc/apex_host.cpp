@@ -768,8 +768,9 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
     apex_status st = plan_step(kv, seq_of_row, lens, plan);
     if (st != APEX_OK) return st;
     // packed upload: header | cta_begin | items (fixed offset) | merges | slots | bt deltas |
-    // len deltas -- one H2D copy of exactly the used bytes; kernels find the merge list and
-    // the slot map through offsets in the header (fixed launch parameters)
+    // len deltas -- exactly the used bytes, moved by one upload (the zero-copy upload kernel, or
+    // an H2D copy with -DAPEX_UPLOAD_KERNEL=0); kernels find the merge list and the slot map
+    // through offsets in the header (fixed launch parameters)
     const size_t items_bytes = sizeof(apex::ItemRec) * plan.items.size();
     const size_t merges_bytes = sizeof(MergeItem) * plan.merges.size();
     const size_t o_merges = align_up(kv->ws.o_items + items_bytes, 256);
@@ -781,7 +782,7 @@ apex_status apex_kv_alloc(apex_kv *kv, const int32_t *seq_ids, const int32_t *n_
         return fail(APEX_EINVAL, "step metadata (%zu B) exceeds the upload region (%zu B)", up_end, kv->ws.upload_cap);
     const int r = kv->ring;
     if (!kv->host_only && kv->staged_pending[r]) {
-        cudaError_t e = cudaEventSynchronize(kv->staged[r]);   // its previous H2D must be done
+        cudaError_t e = cudaEventSynchronize(kv->staged[r]);   // its previous upload must be done
         if (e != cudaSuccess) return cuda_fail(e, "apex_kv_alloc: staging reuse");
         kv->staged_pending[r] = false;
     }
